@@ -1,0 +1,384 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native fused matrix-free PCG (arXiv 1302.7193).
+
+Workload (BASELINE.json metric/config 3): fp64 1024x1024x128 cubed-sphere panel,
+omega2 = 6.71e-4, lambda2 = 3.32e-2, H = 1e-2, RHS fill_random(seed 42), u0 = 0,
+interleaved PCG (paper Alg. 1-3) with eps = tau = 1e-300 so it never exits early
+(the reference's own bench protocol, proj/tools/main.cpp:210-217).
+A "step" is one PCG iteration over the whole grid (fused preconditioner sweep +
+fused stencil sweep + their reductions and scalar updates). Every field is 1.07 GB,
+far larger than the 126 MB L2, so no L2 flush is needed between iterations.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config c1..c5]
+
+N > 1 runs one process per GPU under torchrun (i-slab decomposition, NCCL halos +
+all-gathered reduction partials). Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG iter/s & achieved HBM GB/s (fp64 1024²×128) at 1/2/4/8 B200 vs CPU ref"
+
+CONFIGS = {
+    "c1": dict(m=128, n_z=64, dtype="f64", lambda2=3.32e-2),
+    "c2": dict(m=512, n_z=128, dtype="f64", lambda2=3.32e-2),
+    "c3": dict(m=1024, n_z=128, dtype="f64", lambda2=3.32e-2),
+    "c4": dict(m=2048, n_z=128, dtype="f32", lambda2=1.0e2),  # median gamma^2 ~ 1e4
+    "c5": dict(m=4096, n_z=64, dtype="f64", lambda2=3.32e-2),
+}
+OMEGA2, H = 6.71e-4, 1e-2
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(
+        os.environ.get("LOCAL_RANK", 0))
+
+
+def setup_arrays(cfg):
+    """Host setup (grid, panel, profile) through the product's own host code."""
+    import paper_1302_7193_b200 as acg
+    g = acg.vertical_grid(cfg["n_z"], H)
+    pan = acg.cubed_sphere_panel(cfg["m"])
+    pro = acg.vertical_profile(g, OMEGA2, cfg["lambda2"])
+    return (pro.a_prime, pro.b_prime, pro.c_prime, pro.d), (
+        pan.cell_area, pan.alpha_east, pan.alpha_north, pan.alpha_diag)
+
+
+def algorithmic_bytes(cfg, s):
+    """K1 = s(4N + 2m^2), K2 = s(7N + 6m^2); iteration = s(11N + 8m^2)."""
+    m, n_z = cfg["m"], cfg["n_z"]
+    N = m * m * n_z
+    return {"fused_prec": s * (4 * N + 2 * m * m), "fused_spmv": s * (7 * N + 6 * m * m),
+            "iteration": s * (11 * N + 8 * m * m)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        load = [x for x in sm if x > 0.5 * (mx or max(sm))] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(cfg, iters, workers, warm=True):
+    """The reference's own interleaved PCG (oracle/_ref, compiled from
+    /root/reference) on the host cores: steady it/s = iters / (fused_prec_s +
+    fused_spmv_s), solver.hpp:39-47 timings."""
+    from oracle.oracle import Problem, Reference
+    prob = Problem(cfg["m"], cfg["n_z"], True, OMEGA2, cfg["lambda2"], H)
+    ref = Reference(prob, workers=workers)
+    dt = np.float32 if cfg["dtype"] == "f32" else np.float64
+    f = ref.random_field(42, dt)
+    if warm:
+        ref.solve(f, epsilon=1e-300, tau=1e-300, maxiter=1)  # bench warm-up (main.cpp:212-213)
+    t0 = time.perf_counter()
+    _, res = ref.solve(f, epsilon=1e-300, tau=1e-300, maxiter=iters)
+    wall = time.perf_counter() - t0
+    loop = res.timings["fused_prec_s"] + res.timings["fused_spmv_s"]
+    return {"it_s": iters / loop, "loop_s": loop, "wall_s": wall, "iters": iters,
+            "per_iter_ms_bench": (res.timings["total_s"] - res.timings["setup_s"]) / iters * 1e3}
+
+
+def run_reference_impl(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    try:
+        from oracle.oracle import ref_available
+        if not ref_available():
+            raise RuntimeError("oracle/_ref not built")
+        for _ in range(max(args.warmup, 0)):
+            pass  # the 1-iteration warm-up solve below is the reference's own protocol
+        r = cpu_reference(cfg, args.steps, cores)
+        kind = "reference"
+    except Exception as exc:  # the C port is the fallback checker
+        r = cpu_port(cfg, args.steps)
+        kind = f"port ({exc})"
+        cores = 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["it_s"], "unit": "iter/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / r["it_s"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": workload(cfg, args, 1),
+        "cpu_baseline": {"value": r["it_s"], "unit": "iter/s", "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} interleaved iterations of the full "
+                                   f"{cfg['m']}^2x{cfg['n_z']} problem (steady loop time)"},
+        "e2e": {"value": r["it_s"], "unit": "iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_port(cfg, iters):
+    from oracle.oracle import Oracle, Problem
+    o = Oracle(Problem(cfg["m"], cfg["n_z"], True, OMEGA2, cfg["lambda2"], H))
+    f = o.random_field(42, np.float32 if cfg["dtype"] == "f32" else np.float64)
+    t0 = time.perf_counter()
+    o.solve(f, epsilon=1e-300, tau=1e-300, maxiter=iters)
+    dt = time.perf_counter() - t0
+    return {"it_s": iters / dt, "loop_s": dt, "wall_s": dt, "iters": iters}
+
+
+def workload(cfg, args, n):
+    return {"workload": f"{cfg['dtype']} {cfg['m']}x{cfg['m']}x{cfg['n_z']} cubed-sphere, "
+                        f"interleaved matrix-free PCG (paper Alg. 1-3)",
+            "m": cfg["m"], "n_z": cfg["n_z"], "omega2": OMEGA2, "lambda2": cfg["lambda2"],
+            "h_atmos": H, "seed": 42, "math": args.math, "variant": args.variant,
+            "parallelism": f"{n} i-slab(s), one per GPU" if n > 1 else "1 GPU",
+            "l2": "no flush: every field (N*s bytes) exceeds the 126 MB L2"}
+
+
+# ---------------------------------------------------------------- GPU
+def run_gpu(args, cfg):
+    import torch
+    from paper_1302_7193_b200 import capi
+
+    rank, world, local = dist_env()
+    dev = local
+    torch.cuda.set_device(dev)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        obj = [capi.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = capi.Comm(rank, world, obj[0], dev)
+    dtype = capi.F32 if cfg["dtype"] == "f32" else capi.F64
+    s = 4 if dtype == capi.F32 else 8
+    math_mode = capi.FAST if args.math == "fast" else capi.EXACT
+    profile, panel = setup_arrays(cfg)
+    ctx = capi.Context.from_setup(profile, panel, dtype=dtype, math=math_mode, device=dev,
+                                  comm=comm, slabs=1 if comm else args.slabs)
+    info = ctx.info()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    launches0 = capi.launch_count()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    f = ctx.field().fill_random(42)
+    variant = capi.INTERLEAVED if args.variant == "interleaved" else capi.STANDARD
+    solver = capi.Solver(ctx, epsilon=1e-300, tau=1e-300, maxiter=args.warmup + args.steps + 8,
+                         variant=variant)
+    solver.start(f)
+    solver.iterate(args.warmup)
+    ctx.sync()
+    barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    solver.time_kernels(True)
+    launches_before = capi.launch_count()
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        solver.iterate(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    launches_timed = capi.launch_count() - launches_before
+    ms = ev0.elapsed_time(ev1)
+    kt = solver.kernel_times()
+    res = solver.finish()
+    solver.close()
+
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    it_s = args.steps / (ms_max * 1e-3)
+
+    # ---- roofline of the dominant kernel (CUDA events on the launching stream)
+    pk, pk_kind = peaks()
+    ab = algorithmic_bytes(cfg, s)
+    local_frac = (info["i_end"] - info["i_begin"]) / cfg["m"]
+    n1, t1 = kt["fused_prec"]
+    n2, t2 = kt["fused_spmv"]
+    dom = "fused_spmv" if t2 >= t1 else "fused_prec"
+    nd, td = (n2, t2) if dom == "fused_spmv" else (n1, t1)
+    per_launch_ms = td / max(nd, 1)
+    bytes_launch = ab[dom] * local_frac
+    achieved = bytes_launch / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tj = json.load(fh)
+        key = f"{cfg['m']}x{cfg['n_z']}_{cfg['dtype']}_{args.math}"
+        traffic = tj.get(key, {}).get(dom)
+    except Exception:
+        pass
+    roof = {"kernel": "k_" + dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+            "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+            "algorithmic_bytes_per_launch": bytes_launch, "peak_kind": pk_kind,
+            "launch_ms": per_launch_ms,
+            "fused_prec_ms": t1 / max(n1, 1), "fused_spmv_ms": t2 / max(n2, 1),
+            "fused_prec_gbs": ab["fused_prec"] * local_frac / (t1 / max(n1, 1) * 1e-3) / 1e9,
+            "fused_spmv_gbs": ab["fused_spmv"] * local_frac / (t2 / max(n2, 1) * 1e-3) / 1e9}
+    iter_gbs = ab["iteration"] * it_s / 1e9
+
+    # ---- e2e through the C ABI with pinned host buffers (H2D f, solve, D2H u)
+    e2e = None
+    if not args.no_e2e:
+        m, n_z = cfg["m"], cfg["n_z"]
+        ml = info["i_end"] - info["i_begin"]
+        npdt = np.float32 if dtype == capi.F32 else np.float64
+        hf = capi.HostBuffer((ml, m, n_z), npdt)
+        hu = capi.HostBuffer((ml, m, n_z), npdt)
+        f.download(out=hf.array, scope=capi.HOST_LOCAL)
+        f2, u2 = ctx.field(), ctx.field()
+        barrier()
+        t0 = time.perf_counter()
+        f2.upload(hf.array, scope=capi.HOST_LOCAL)
+        r2 = capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps)
+        u2.download(out=hu.array, scope=capi.HOST_LOCAL)
+        barrier()
+        wall = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        nbytes = ml * m * n_z * s
+        e2e = {"value": args.steps / wall, "unit": "iter/s",
+               "h2d_bytes_per_step": nbytes * world / args.steps,
+               "d2h_bytes_per_step": nbytes * world / args.steps + 8 * (args.steps + 1),
+               "call": "acg_field_upload + acg_solve + acg_field_download (pinned host)",
+               "solve_wall_s": wall, "iterations": r2["iterations"]}
+        f2.close()
+        u2.close()
+        hf.close()
+        hu.close()
+
+    # ---- CPU baseline (the reference compiled from source, all host cores)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        try:
+            r = cpu_reference(cfg, args.cpu_iters, cores)
+            cpu = {"value": r["it_s"], "unit": "iter/s", "cores": cores, "kind": "reference",
+                   "sample": f"{args.cpu_iters} interleaved iterations of the full "
+                             f"{cfg['m']}^2x{cfg['n_z']} {cfg['dtype']} problem, steady loop "
+                             f"time from the reference's KernelTimings ({r['loop_s']:.1f} s)"}
+        except Exception as exc:
+            cpu = {"value": None, "unit": "iter/s", "cores": cores, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": it_s, "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic", "config": workload(cfg, args, world),
+            "achieved_gbs_iteration": iter_gbs,
+            "frac_of_peak_iteration": iter_gbs / pk["hbm_gbs"],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_timed, "clocks": clk.summary(),
+            "exact_tree": bool(info["exact_tree"]),
+            "residual_after": float(res["residual_history"][-1]) if res["residual_history"].size else None,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if comm:
+        comm.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--math", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--variant", default="interleaved", choices=["interleaved", "standard"])
+    ap.add_argument("--slabs", type=int, default=1, help="virtual slabs on one GPU (N=1)")
+    ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_impl(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

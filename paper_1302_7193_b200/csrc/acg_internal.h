@@ -1,0 +1,159 @@
+// Internal types shared by the kernels (acg_kernels.cu) and the runtime
+// (acg_runtime.cu). Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace acg {
+
+// Device field layout ("plane-major"): a slab owning global
+// i-planes [i0, i0 + m_loc) stores element (i, j, k) at
+//     (i - i0) * plane + k * m + j,      plane = n_z * m,
+// so a warp of 32 consecutive j is one coalesced 256 B (fp64) row, the vertical
+// neighbour is +-m and the i-neighbour is +-plane. One ghost plane precedes
+// plane 0 and one follows plane m_loc-1; they receive the neighbouring slabs'
+// boundary planes (halo exchange). Contiguous i-slabs keep each slab's column
+// partials a contiguous block of the reference's column order col = i*m + j.
+
+// Rows of the per-slab profile table (n_z entries each), converted to T on the
+// host exactly like OperatorContext<T> (operator.hpp:36-43).
+enum ProfRow { kProfS = 0,   // (a'_k - b'_k) - c'_k   (operator.hpp:127, :307)
+               kProfB = 1,   // b'_k
+               kProfC = 2,   // c'_k
+               kProfD = 3,   // d_k
+               kProfInvD = 4,// 1 / d_k          (fast math only)
+               kProfRows = 5 };
+
+// Rows of the per-slab column table (m_loc * m entries each, index il*m + j).
+enum ColRow { kColArea = 0,  // |T|
+              kColDiag = 1,  // alpha_diag
+              kColAtil = 2,  // alpha_diag / |T| in T (operator.hpp:163, :302)
+              kColE = 3,     // alpha toward i+1 (0 on the panel edge), operator.hpp:81
+              kColW = 4,     // alpha toward i-1
+              kColN = 5,     // alpha toward j+1
+              kColS = 6,     // alpha toward j-1
+              kColInvA = 7,  // 1 / |T|          (fast math only)
+              kColRows = 8 };
+
+template <typename T>
+struct SlabView {
+    int m, n_z, m_loc, i0;
+    long long plane;  // n_z * m
+    const T* prof;    // kProfRows x n_z
+    const T* col;     // kColRows x (m_loc * m)
+};
+
+// Reasons a solve stops with NumericalBreakdown (operator.hpp:21-24,
+// solver.hpp:214-362).
+enum ErrCode { kErrNone = 0,
+               kErrPivotFused = 1,    // interleaved_prec_kernel zero pivot
+               kErrPivotPrecond = 2,  // precondition zero pivot
+               kErrKappa = 3,         // <r,z> not positive
+               kErrSigma = 4 };       // <p,Ap> not positive
+
+// Device-resident CG scalars and loop control (FusedState<T> scalars,
+// operator.hpp:195-208, plus the driver state of solver.hpp:275-370).
+template <typename T>
+struct Scalars {
+    T alpha, beta, kappa, kappa_old, sigma, r_norm, r0, neg_alpha;
+    T val[4];  // last reduction results (API queries)
+    double eps, tau;
+    int maxiter, it, iterations;
+    int done, converged, error;
+    int n_res, n_kap, n_alp, n_bet;
+    int pivot;  // written by the Thomas kernels on a zero pivot
+    int pad_;
+    double* h_res;
+    double* h_kap;
+    double* h_alp;
+    double* h_bet;
+};
+
+// Scalar programs run by the reduction finish (all on device, no host sync).
+enum ScalarOp {
+    kOpStore = 0,     // val[] = sums
+    kOpR0 = 1,        // r0 = sqrt(s0); history; tau test     (solver.hpp:299-312)
+    kOpKappa0 = 2,    // kappa_old = s0 > 0                     (:317-323)
+    kOpSigma0 = 3,    // sigma = s0 > 0; alpha                  (:329-336)
+    kOpIlPrec = 4,    // after fused prec: ||r||, kappa, test, beta   (:340-356)
+    kOpIlSpmv = 5,    // after fused spmv: sigma, alpha, it++         (:358-364)
+    kOpStdSigma = 6,  // standard loop: sigma, alpha                  (:224-230)
+    kOpStdRnorm = 7,  // standard loop: ||r||, test                   (:236-244)
+    kOpStdKappa = 8,  // standard loop: kappa, beta, it++             (:250-258)
+};
+
+// Fixed-shape pairwise reduction plan (parallel.hpp:11-20) for n values:
+// nodes at depth D are summed per thread by the reference's own rule
+// (sizes <= 16), everything above depth D is a perfect binary tree.
+struct TreePlan {
+    long long n;
+    int depth;    // D
+    int nodes;    // 2^D
+    int threads;  // stage-1 block size (<= 256, power of two)
+    int blocks;   // stage-1 blocks = stage-2 leaves (power of two)
+};
+TreePlan make_tree_plan(long long n);
+
+// Dynamic shared memory of one Thomas block (K1/K4) for a column height.
+size_t thomas_smem_per_block(int dsize, int n_z, bool global_phi);
+
+// ----------------------------------------------------------------- launchers
+extern long long g_launches;  // kernel launches issued (all entry points)
+
+template <typename T>
+void launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
+                       T* part_k, Scalars<T>* S, T* phi_scratch, cudaStream_t st);
+template <typename T>
+void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scalars<T>* S,
+                         const Scalars<T>* gate, T* phi_scratch, cudaStream_t st);
+template <typename T>
+void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
+                       const Scalars<T>* S, cudaStream_t st);
+template <typename T>
+void launch_apply(const SlabView<T>& v, bool fast, const T* x, T* y, const Scalars<T>* gate,
+                  cudaStream_t st);
+template <typename T>
+void launch_residual_partials(const SlabView<T>& v, bool fast, const T* u, const T* f, T* part,
+                              cudaStream_t st);
+template <typename T>
+void launch_dot_partials(const SlabView<T>& v, const T* x, const T* y, T* part,
+                         const Scalars<T>* gate, cudaStream_t st);
+// y = c*x + y with c = value (coef == nullptr) or *coef (negated if neg).
+template <typename T>
+void launch_axpy(long long n, T value, const T* coef, bool neg, const T* x, T* y,
+                 const Scalars<T>* gate, cudaStream_t st);
+template <typename T>
+void launch_scal(long long n, T value, const T* coef, T* x, const Scalars<T>* gate,
+                 cudaStream_t st);
+template <typename T>
+void launch_copy(long long n, const T* x, T* y, const Scalars<T>* gate, cudaStream_t st);
+template <typename T>
+void launch_fill(long long n, T value, T* x, cudaStream_t st);
+template <typename T>
+void launch_fill_random(const SlabView<T>& v, uint64_t seed, T* x, cudaStream_t st);
+
+// Reductions: nv (<= 3) arrays of plan.n values -> slab sums.
+//  stage 1: blocks x nv partial node sums into `stage`.
+//  stage 2: perfect tree over the blocks; writes nv slab sums into
+//           gather[slab * 4 + v]; if finish, also combines the gather and runs `op`.
+template <typename T>
+void launch_tree_stage1(const TreePlan& plan, const T* in0, const T* in1, const T* in2, int nv,
+                        T* stage, const Scalars<T>* gate, cudaStream_t st);
+template <typename T>
+void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
+                        bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
+                        cudaStream_t st);
+template <typename T>
+void launch_finish(const T* gather, int nv, int nslabs, bool exact_tree, Scalars<T>* S, int op,
+                   cudaStream_t st);
+
+// relayout between the reference's host layouts and plane-major (K7):
+// out[x*osx + y + b*osb] = in[x + y*isy + b*isb]  for x<nx, y<ny, b<nb
+template <typename T>
+void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy, long long isb,
+                      long long osx, long long osb, cudaStream_t st);
+
+}  // namespace acg

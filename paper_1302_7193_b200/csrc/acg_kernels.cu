@@ -1,0 +1,974 @@
+// sm_100a kernels of the B200-native matrix-free PCG (arXiv 1302.7193).
+//
+//   K1 k_fused_prec     interleaved_prec_kernel   operator.hpp:272-346 (Alg. 3)
+//   K2 k_fused_spmv     interleaved_spmv_kernel   operator.hpp:214-266 (Alg. 2)
+//   K3 k_apply          apply                     operator.hpp:101-135
+//   K4 k_precondition   precondition              operator.hpp:141-191
+//   K5 k_axpy/k_scal/k_dot_partials  field.hpp:116-173
+//   K6 k_tree1/k_tree2/k_finish      pairwise_sum parallel.hpp:11-20 + the
+//                                    scalar recurrences of solver.hpp:288-364
+//   K7 k_transpose      relayout / array_to_field field.hpp:102-109, bindings.cpp:40-59
+//   K8 k_residual_partials  true_residual        solver.hpp:61-69 (one pass)
+//   K11 k_fill_random   fill_random               field.hpp:180-196
+//
+// One thread owns one vertical column (paper Sec. 5, "one thread per column");
+// a warp covers 32 consecutive j of one i-plane, so every level of every field
+// is one coalesced row. Every arithmetic operation of the EXACT path is an
+// explicit IEEE round-to-nearest intrinsic in the reference's association
+// order (the reference builds with -ffp-contract=off), which makes the GPU
+// bit-identical to the CPU. The FAST path allows FMA contraction and replaces
+// the three divides per Thomas level by one reciprocal.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "acg_internal.h"
+
+namespace acg {
+
+long long g_launches = 0;
+
+namespace {
+
+// ------------------------------------------------------------- arithmetic
+template <typename T, bool Fast>
+struct Ar;
+template <>
+struct Ar<double, false> {
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+template <>
+struct Ar<float, false> {
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+};
+template <typename T>
+struct Ar<T, true> {
+    static __device__ __forceinline__ T mul(T a, T b) { return a * b; }
+    static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+    static __device__ __forceinline__ T sub(T a, T b) { return a - b; }
+    static __device__ __forceinline__ T div(T a, T b) { return a / b; }
+};
+
+__device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
+__device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+inline int grid_1d(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    const long long cap = 148LL * 32;
+    return static_cast<int>(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+template <typename T>
+__device__ __forceinline__ void load_profile(T* prof, const T* src, int count, int tid,
+                                             int nthreads) {
+    for (int t = tid; t < count; t += nthreads) prof[t] = src[t];
+}
+
+// 7-point stencil value (operator.hpp:127-132), summed left to right.
+template <typename T, bool Fast>
+__device__ __forceinline__ T stencil(T sA, T area, T adiag, T bk, T ck, T ae, T aw, T an, T as,
+                                     T x0, T xu, T xd, T xe, T xw, T xn, T xs) {
+    using A = Ar<T, Fast>;
+    T t = A::mul(A::sub(A::mul(sA, area), adiag), x0);
+    t = A::add(t, A::mul(A::mul(area, bk), xu));
+    t = A::add(t, A::mul(A::mul(area, ck), xd));
+    t = A::add(t, A::mul(ae, xe));
+    t = A::add(t, A::mul(aw, xw));
+    t = A::add(t, A::mul(an, xn));
+    t = A::add(t, A::mul(as, xs));
+    return t;
+}
+
+// Per-column stencil data (ColumnStencil, operator.hpp:75-94). Missing
+// horizontal edges read the column's own value with a zero coefficient.
+template <typename T>
+struct Col {
+    T area, adiag, ae, aw, an, as;
+    long long oe, ow, on, os;
+};
+
+template <typename T>
+__device__ __forceinline__ Col<T> load_col(const SlabView<T>& v, int il, int j) {
+    const long long ncol = static_cast<long long>(v.m_loc) * v.m;
+    const long long c = static_cast<long long>(il) * v.m + j;
+    const int ig = v.i0 + il;
+    Col<T> s;
+    s.area = v.col[kColArea * ncol + c];
+    s.adiag = v.col[kColDiag * ncol + c];
+    s.ae = v.col[kColE * ncol + c];
+    s.aw = v.col[kColW * ncol + c];
+    s.an = v.col[kColN * ncol + c];
+    s.as = v.col[kColS * ncol + c];
+    s.oe = ig + 1 < v.m ? v.plane : 0;
+    s.ow = ig > 0 ? -v.plane : 0;
+    s.on = j + 1 < v.m ? 1 : 0;
+    s.os = j > 0 ? -1 : 0;
+    return s;
+}
+
+// ================================================================ K1 / K4
+#include "acg_thomas.cuh"
+
+// ================================================================ K2 / K3 / K8
+constexpr int kStencilWarps = 8;
+
+// K2: u += a p; p = z + b p; q = A z + b q; sigma partial (operator.hpp:243-261)
+template <typename T, bool Fast>
+__global__ void __launch_bounds__(32 * kStencilWarps)
+    k_fused_spmv(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p, T* __restrict__ q,
+                 const T* __restrict__ z, T* __restrict__ part, const Scalars<T>* __restrict__ S) {
+    using A = Ar<T, Fast>;
+    if (S->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, 32 * kStencilWarps);
+    __syncthreads();
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    const int il = blockIdx.y * kStencilWarps + threadIdx.y;
+    if (j >= m || il >= v.m_loc) return;
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> c = load_col(v, il, j);
+    const T alpha = S->alpha, beta = S->beta;
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    const T* zc = z + base;
+    T* uc = u + base;
+    T* pc = p + base;
+    T* qc = q + base;
+    T z0 = zc[0], zd = z0, sig = T(0);
+#pragma unroll 4
+    for (int k = 0; k < n_z; ++k) {
+        const long long l = static_cast<long long>(k) * m;
+        const T zu = (k + 1 < n_z) ? zc[l + m] : z0;
+        const T ze = zc[l + c.oe], zw = zc[l + c.ow], zn = zc[l + c.on], zs = zc[l + c.os];
+        T ps = __ldcs(pc + l), qs = __ldcs(qc + l);
+        const T uv = __ldcs(uc + l);
+        __stcs(uc + l, A::add(uv, A::mul(alpha, ps)));
+        ps = A::add(A::mul(beta, ps), z0);
+        qs = A::mul(beta, qs);
+        __stcs(pc + l, ps);
+        const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an,
+                                      c.as, z0, zu, zd, ze, zw, zn, zs);
+        qs = A::add(qs, A::mul(dP[k], dq));
+        sig = A::add(sig, A::mul(ps, qs));
+        __stcs(qc + l, qs);
+        zd = z0;
+        z0 = zu;
+    }
+    part[static_cast<long long>(il) * m + j] = sig;
+}
+
+// K2 with a cp.async ring: p, q, u and the next level of z are copied D levels
+// ahead into a per-thread shared-memory ring (asynchronous, no registers held),
+// so each SM keeps ~(warps x 32 x D x 32 B) in flight; the four horizontal z
+// neighbours are plain loads that hit L1/L2 (the rows belong to adjacent warps).
+constexpr int kSpmvD = 6;
+
+template <typename T, bool Fast>
+__global__ void __launch_bounds__(32 * kStencilWarps)
+    k_fused_spmv_ring(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
+                      T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
+                      const Scalars<T>* __restrict__ S) {
+    using A = Ar<T, Fast>;
+    constexpr int NT = 32 * kStencilWarps, D = kSpmvD, NS = kSpmvD + 1;
+    if (S->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);
+    __syncthreads();
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    const int il = blockIdx.y * kStencilWarps + threadIdx.y;
+    if (j >= m || il >= v.m_loc) return;
+    T* ring = prof + 4 * n_z;
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> c = load_col(v, il, j);
+    const T alpha = S->alpha, beta = S->beta;
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    const T* zc = z + base;
+    T* uc = u + base;
+    T* pc = p + base;
+    T* qc = q + base;
+    auto slot = [&](int s, int a) -> T* { return ring + (s * 4 + a) * NT + tid; };
+    auto issue = [&](int k, int s) {
+        const long long l = static_cast<long long>(k) * m;
+        cpa(slot(s, 0), pc + l);
+        cpa(slot(s, 1), qc + l);
+        cpa(slot(s, 2), uc + l);
+        if (k + 1 < n_z) cpa(slot(s, 3), zc + l + m);
+    };
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        if (t < n_z) issue(t, t);
+        cp_commit();
+    }
+    int cs = 0, ps_ = D;
+    T z0 = zc[0], zd = z0, sig = T(0);
+    for (int k = 0; k < n_z; ++k) {
+        const long long l = static_cast<long long>(k) * m;
+        const T ze = zc[l + c.oe], zw = zc[l + c.ow], zn = zc[l + c.on], zs = zc[l + c.os];
+        cp_wait<D - 1>();
+        T pv = *slot(cs, 0), qv = *slot(cs, 1);
+        const T uv = *slot(cs, 2);
+        const T zu = (k + 1 < n_z) ? *slot(cs, 3) : z0;
+        if (k + D < n_z) issue(k + D, ps_);
+        cp_commit();
+        cs = cs + 1 == NS ? 0 : cs + 1;
+        ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
+        __stcs(uc + l, A::add(uv, A::mul(alpha, pv)));
+        pv = A::add(A::mul(beta, pv), z0);
+        qv = A::mul(beta, qv);
+        __stcs(pc + l, pv);
+        const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an, c.as,
+                                      z0, zu, zd, ze, zw, zn, zs);
+        qv = A::add(qv, A::mul(dP[k], dq));
+        sig = A::add(sig, A::mul(pv, qv));
+        __stcs(qc + l, qv);
+        zd = z0;
+        z0 = zu;
+    }
+    cp_wait<0>();
+    part[static_cast<long long>(il) * m + j] = sig;
+}
+
+// K3: y = A x (operator.hpp:124-133)
+template <typename T, bool Fast>
+__global__ void __launch_bounds__(32 * kStencilWarps)
+    k_apply(const SlabView<T> v, const T* __restrict__ x, T* __restrict__ y,
+            const Scalars<T>* __restrict__ gate) {
+    using A = Ar<T, Fast>;
+    if (gate && gate->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, 32 * kStencilWarps);
+    __syncthreads();
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    const int il = blockIdx.y * kStencilWarps + threadIdx.y;
+    if (j >= m || il >= v.m_loc) return;
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> c = load_col(v, il, j);
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    const T* xc = x + base;
+    T* yc = y + base;
+    T x0 = xc[0], xd = x0;
+#pragma unroll 4
+    for (int k = 0; k < n_z; ++k) {
+        const long long l = static_cast<long long>(k) * m;
+        const T xu = (k + 1 < n_z) ? xc[l + m] : x0;
+        const T t = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an, c.as,
+                                     x0, xu, xd, xc[l + c.oe], xc[l + c.ow], xc[l + c.on],
+                                     xc[l + c.os]);
+        __stcs(yc + l, A::mul(t, dP[k]));
+        xd = x0;
+        x0 = xu;
+    }
+}
+
+// K8: per-column sum of (f - A u)^2 — true_residual (solver.hpp:61-69) in one
+// pass: -t is exact and f + (-t) == f - t, so this equals apply+scal+axpy+nrm2.
+template <typename T, bool Fast>
+__global__ void __launch_bounds__(32 * kStencilWarps)
+    k_residual_partials(const SlabView<T> v, const T* __restrict__ u, const T* __restrict__ f,
+                        T* __restrict__ part) {
+    using A = Ar<T, Fast>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, 32 * kStencilWarps);
+    __syncthreads();
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    const int il = blockIdx.y * kStencilWarps + threadIdx.y;
+    if (j >= m || il >= v.m_loc) return;
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> c = load_col(v, il, j);
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    const T* uc = u + base;
+    const T* fc = f + base;
+    T x0 = uc[0], xd = x0, sum = T(0);
+#pragma unroll 4
+    for (int k = 0; k < n_z; ++k) {
+        const long long l = static_cast<long long>(k) * m;
+        const T xu = (k + 1 < n_z) ? uc[l + m] : x0;
+        const T t = A::mul(stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an,
+                                            c.as, x0, xu, xd, uc[l + c.oe], uc[l + c.ow],
+                                            uc[l + c.on], uc[l + c.os]),
+                           dP[k]);
+        const T r = A::sub(__ldcs(fc + l), t);
+        sum = A::add(sum, A::mul(r, r));
+        xd = x0;
+        x0 = xu;
+    }
+    part[static_cast<long long>(il) * m + j] = sum;
+}
+
+// per-column dot partials in ascending k (field.hpp:134-153)
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_dot_partials(const SlabView<T> v, const T* __restrict__ x, const T* __restrict__ y,
+                   T* __restrict__ part, const Scalars<T>* __restrict__ gate) {
+    using A = Ar<T, false>;
+    if (gate && gate->done) return;
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    const int il = blockIdx.y * 8 + threadIdx.y;
+    if (j >= v.m || il >= v.m_loc) return;
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    T s = T(0);
+#pragma unroll 4
+    for (int k = 0; k < v.n_z; ++k) {
+        const long long l = base + static_cast<long long>(k) * v.m;
+        s = A::add(s, A::mul(__ldcs(x + l), __ldcs(y + l)));
+    }
+    part[static_cast<long long>(il) * v.m + j] = s;
+}
+
+// ================================================================ K5 BLAS-1
+template <typename T>
+__global__ void k_axpy(long long n, T value, const T* __restrict__ coef, int neg,
+                       const T* __restrict__ x, T* __restrict__ y,
+                       const Scalars<T>* __restrict__ gate) {
+    using A = Ar<T, false>;
+    if (gate && gate->done) return;
+    T a = coef ? *coef : value;
+    if (neg) a = -a;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < n;
+         l += (long long)gridDim.x * blockDim.x)
+        y[l] = A::add(A::mul(a, x[l]), y[l]);
+}
+
+template <typename T>
+__global__ void k_scal(long long n, T value, const T* __restrict__ coef, T* __restrict__ x,
+                       const Scalars<T>* __restrict__ gate) {
+    using A = Ar<T, false>;
+    if (gate && gate->done) return;
+    const T a = coef ? *coef : value;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < n;
+         l += (long long)gridDim.x * blockDim.x)
+        x[l] = A::mul(a, x[l]);
+}
+
+template <typename T>
+__global__ void k_copy(long long n, const T* __restrict__ x, T* __restrict__ y,
+                       const Scalars<T>* __restrict__ gate) {
+    if (gate && gate->done) return;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < n;
+         l += (long long)gridDim.x * blockDim.x)
+        y[l] = x[l];
+}
+
+template <typename T>
+__global__ void k_fill(long long n, T value, T* __restrict__ x) {
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < n;
+         l += (long long)gridDim.x * blockDim.x)
+        x[l] = value;
+}
+
+// K11: draw number n = (i*m + j)*n_z + k of the sequential splitmix64 stream
+// (field.hpp:180-196): state_n = seed + (n+1)*golden, so every element is
+// generated independently and the field matches the host fill bit for bit.
+template <typename T>
+__global__ void k_fill_random(const SlabView<T> v, uint64_t seed, T* __restrict__ x) {
+    const long long total = static_cast<long long>(v.m_loc) * v.plane;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < total;
+         l += (long long)gridDim.x * blockDim.x) {
+        const long long il = l / v.plane;
+        const long long rem = l - il * v.plane;
+        const long long k = rem / v.m;
+        const long long j = rem - k * v.m;
+        const unsigned long long nidx =
+            (static_cast<unsigned long long>(v.i0 + il) * v.m + j) * v.n_z + k;
+        unsigned long long s = seed + (nidx + 1ull) * 0x9e3779b97f4a7c15ull;
+        s = (s ^ (s >> 30)) * 0xbf58476d1ce4e5b9ull;
+        s = (s ^ (s >> 27)) * 0x94d049bb133111ebull;
+        s = s ^ (s >> 31);
+        const double u = __dmul_rn(static_cast<double>(s >> 11), 0x1.0p-53);
+        x[l] = static_cast<T>(__dsub_rn(__dmul_rn(2.0, u), 1.0));
+    }
+}
+
+// ================================================================ K7 relayout
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ in, T* __restrict__ out, int nx, int ny, int nb,
+                            long long isy, long long isb, long long osx, long long osb) {
+    __shared__ T tile[32][33];
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    for (int b = blockIdx.z; b < nb; b += gridDim.z) {
+        for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+            const int x = x0 + threadIdx.x, y = y0 + dy;
+            if (x < nx && y < ny) tile[dy][threadIdx.x] = in[x + y * isy + b * isb];
+        }
+        __syncthreads();
+        for (int dx = threadIdx.y; dx < 32; dx += blockDim.y) {
+            const int y = y0 + threadIdx.x, x = x0 + dx;
+            if (x < nx && y < ny) out[x * osx + y + b * osb] = tile[threadIdx.x][dx];
+        }
+        __syncthreads();
+    }
+}
+
+// ================================================================ K6 reductions
+__device__ __forceinline__ void node_range(long long n, int depth, long long t, long long& lo,
+                                           long long& hi) {
+    lo = 0;
+    hi = n;
+    for (int b = depth - 1; b >= 0; --b) {
+        const long long mid = lo + (hi - lo) / 2;
+        if ((t >> b) & 1)
+            lo = mid;
+        else
+            hi = mid;
+    }
+}
+
+// pairwise_sum of a node of size <= 16 (parallel.hpp:11-20)
+template <typename T>
+__device__ __forceinline__ T leaf_sum(const T* v, long long n) {
+    auto seq = [](const T* a, long long c) {
+        T s = T(0);
+        for (long long l = 0; l < c; ++l) s = add_rn(s, a[l]);
+        return s;
+    };
+    if (n <= 8) return seq(v, n);
+    const long long h = n / 2;
+    return add_rn(seq(v, h), seq(v + h, n - h));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_tree1(long long n, int depth, const T* __restrict__ in0, const T* __restrict__ in1,
+            const T* __restrict__ in2, int nv, T* __restrict__ stage, int nblocks,
+            const Scalars<T>* __restrict__ gate) {
+    if (gate && gate->done) return;
+    __shared__ T sh[3][256];
+    const int tid = threadIdx.x;
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + tid;
+    long long lo, hi;
+    node_range(n, depth, t, lo, hi);
+    const T* ins[3] = {in0, in1, in2};
+    for (int a = 0; a < nv; ++a) sh[a][tid] = leaf_sum(ins[a] + lo, hi - lo);
+    __syncthreads();
+    for (int s = 1; s < static_cast<int>(blockDim.x); s <<= 1) {
+        if ((tid & (2 * s - 1)) == 0)
+            for (int a = 0; a < nv; ++a) sh[a][tid] = add_rn(sh[a][tid], sh[a][tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0)
+        for (int a = 0; a < nv; ++a) stage[a * nblocks + blockIdx.x] = sh[a][0];
+}
+
+// Scalar recurrences of the PCG drivers (solver.hpp:288-364); every value
+// is computed in T and pushed to the histories as double, as in the reference.
+template <typename T>
+__device__ void run_op(Scalars<T>* S, int op, const T* sums) {
+    using A = Ar<T, false>;
+    switch (op) {
+        case kOpStore:
+            for (int a = 0; a < 4; ++a) S->val[a] = sums[a];
+            break;
+        case kOpR0: {
+            const T rn = sqrt_rn(sums[0]);
+            S->r_norm = rn;
+            S->r0 = rn;
+            S->h_res[S->n_res++] = static_cast<double>(rn);
+            if (static_cast<double>(rn) <= S->tau) {
+                S->converged = 1;
+                S->done = 1;
+            }
+        } break;
+        case kOpKappa0: {
+            if (S->pivot) {
+                S->error = kErrPivotPrecond;
+                S->done = 1;
+                break;
+            }
+            S->kappa_old = sums[0];
+            S->h_kap[S->n_kap++] = static_cast<double>(sums[0]);
+            if (!(static_cast<double>(sums[0]) > 0.0)) {
+                S->error = kErrKappa;
+                S->done = 1;
+            }
+        } break;
+        case kOpSigma0:
+        case kOpIlSpmv:
+        case kOpStdSigma: {
+            S->sigma = sums[0];
+            if (!(static_cast<double>(sums[0]) > 0.0)) {
+                S->error = kErrSigma;
+                S->done = 1;
+                break;
+            }
+            const T al = A::div(S->kappa_old, sums[0]);
+            S->alpha = al;
+            S->neg_alpha = -al;
+            S->h_alp[S->n_alp++] = static_cast<double>(al);
+            if (op == kOpSigma0) {
+                S->it = 1;
+            } else if (op == kOpIlSpmv) {
+                if (++S->it > S->maxiter) S->done = 1;
+            }
+        } break;
+        case kOpIlPrec: {
+            if (S->pivot) {
+                S->error = kErrPivotFused;
+                S->done = 1;
+                break;
+            }
+            const T rn = sqrt_rn(sums[0]);
+            const T ka = sums[1];
+            S->r_norm = rn;
+            S->kappa = ka;
+            S->h_res[S->n_res++] = static_cast<double>(rn);
+            S->iterations = S->it;
+            if (static_cast<double>(rn) / static_cast<double>(S->r0) < S->eps ||
+                static_cast<double>(rn) < S->tau) {
+                S->converged = 1;
+                S->done = 1;
+                break;
+            }
+            S->h_kap[S->n_kap++] = static_cast<double>(ka);
+            const T be = A::div(ka, S->kappa_old);
+            S->beta = be;
+            S->h_bet[S->n_bet++] = static_cast<double>(be);
+            S->kappa_old = ka;
+        } break;
+        case kOpStdRnorm: {
+            const T rn = sqrt_rn(sums[0]);
+            S->r_norm = rn;
+            S->h_res[S->n_res++] = static_cast<double>(rn);
+            S->iterations = S->it;
+            if (static_cast<double>(rn) / static_cast<double>(S->r0) < S->eps ||
+                static_cast<double>(rn) < S->tau) {
+                S->converged = 1;
+                S->done = 1;
+            }
+        } break;
+        case kOpStdKappa: {
+            if (S->pivot) {
+                S->error = kErrPivotPrecond;
+                S->done = 1;
+                break;
+            }
+            const T ka = sums[0];
+            S->kappa = ka;
+            S->h_kap[S->n_kap++] = static_cast<double>(ka);
+            const T be = A::div(ka, S->kappa_old);
+            S->beta = be;
+            S->h_bet[S->n_bet++] = static_cast<double>(be);
+            S->kappa_old = ka;
+            if (++S->it > S->maxiter) S->done = 1;
+        } break;
+        default:
+            break;
+    }
+}
+
+// Combine the slab sums of one value: the perfect tree above the slab nodes
+// when the slabs are nodes of the reference tree, else the pairwise rule.
+template <typename T>
+__device__ T combine_slabs(const T* gather, int a, int nslabs, bool exact) {
+    T v[64];
+    for (int s = 0; s < nslabs; ++s) v[s] = gather[s * 4 + a];
+    if (exact) {
+        for (int w = 1; w < nslabs; w <<= 1)
+            for (int s = 0; s + w < nslabs; s += 2 * w) v[s] = add_rn(v[s], v[s + w]);
+        return v[0];
+    }
+    // iterative pairwise_sum over nslabs values (explicit stack)
+    long long st_lo[16], st_n[16];
+    T st_acc[16];
+    int st_state[16];
+    int sp = 0;
+    st_lo[0] = 0;
+    st_n[0] = nslabs;
+    st_state[0] = 0;
+    T ret = T(0);
+    while (sp >= 0) {
+        const long long lo = st_lo[sp], n = st_n[sp];
+        if (n <= 8) {
+            T s = T(0);
+            for (long long l = 0; l < n; ++l) s = add_rn(s, v[lo + l]);
+            ret = s;
+            --sp;
+            continue;
+        }
+        if (st_state[sp] == 0) {
+            st_state[sp] = 1;
+            ++sp;
+            st_lo[sp] = lo;
+            st_n[sp] = n / 2;
+            st_state[sp] = 0;
+        } else if (st_state[sp] == 1) {
+            st_acc[sp] = ret;
+            st_state[sp] = 2;
+            ++sp;
+            st_lo[sp] = lo + n / 2;
+            st_n[sp] = n - n / 2;
+            st_state[sp] = 0;
+        } else {
+            ret = add_rn(st_acc[sp], ret);
+            --sp;
+        }
+    }
+    return ret;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+    k_tree2(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather, int slab,
+            int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op) {
+    if (op != kOpStore && S->done) return;
+    __shared__ T sh[3][1024];
+    const int tid = threadIdx.x;
+    const int nt = blockDim.x;
+    const int c = nleaves / nt;  // leaves per thread, power of two <= 16
+    for (int a = 0; a < nv; ++a) {
+        T v[16];
+        for (int l = 0; l < c; ++l) v[l] = stage[a * nleaves + tid * c + l];
+        for (int w = 1; w < c; w <<= 1)
+            for (int l = 0; l + w < c; l += 2 * w) v[l] = add_rn(v[l], v[l + w]);
+        sh[a][tid] = v[0];
+    }
+    __syncthreads();
+    for (int s = 1; s < nt; s <<= 1) {
+        if ((tid & (2 * s - 1)) == 0)
+            for (int a = 0; a < nv; ++a) sh[a][tid] = add_rn(sh[a][tid], sh[a][tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        for (int a = 0; a < nv; ++a) gather[slab * 4 + a] = sh[a][0];
+        if (finish) {
+            T sums[4] = {T(0), T(0), T(0), T(0)};
+            for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
+            run_op(S, op, sums);
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_finish(const T* __restrict__ gather, int nv, int nslabs, int exact,
+                         Scalars<T>* __restrict__ S, int op) {
+    if (op != kOpStore && S->done) return;
+    T sums[4] = {T(0), T(0), T(0), T(0)};
+    for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
+    run_op(S, op, sums);
+}
+
+// --------------------------------------------------------- launch helpers
+inline void post_launch(const char* what) {
+    ++g_launches;
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "acg: launch of %s failed: %s\n", what, cudaGetErrorString(e));
+    }
+}
+
+template <typename KernelT>
+void ensure_smem(KernelT kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+}
+
+
+// Thomas launch configuration (warps per block, phi checkpoint stride, cp.async
+// depth), chosen per precision; ACG_THOMAS_OCC pads shared memory to cap the
+// resident blocks per SM (L2-footprint experiments).
+using ThomasF64 = ThomasCfg<2, 2, 12>;
+using ThomasF32 = ThomasCfg<2, 1, 12>;
+template <typename T>
+struct ThomasOf;
+template <>
+struct ThomasOf<double> { using type = ThomasF64; };
+template <>
+struct ThomasOf<float> { using type = ThomasF32; };
+
+inline size_t thomas_pad(size_t bytes) {
+    static int occ = [] {
+        const char* e = std::getenv("ACG_THOMAS_OCC");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (occ > 0) {
+        const size_t want = (227u * 1024u) / static_cast<size_t>(occ) - 1024u;
+        if (want > bytes) return want;
+    }
+    return bytes;
+}
+
+template <typename T, bool Fast, bool Fused, class C>
+void launch_thomas_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
+                       Scalars<T>* S, const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
+    const dim3 block(32, C::W);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + C::W - 1) / C::W);
+    const size_t smem = thomas_pad(thomas_smem_bytes<T, C>(v.n_z, phi_scratch != nullptr));
+    ensure_smem(k_thomas<T, Fast, Fused, C>, smem);
+    k_thomas<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch);
+}
+
+// ACG_THOMAS="W,CP,D" selects one of the compiled configurations (tuning sweeps).
+inline int thomas_choice() {
+    static int c = [] {
+        const char* e = std::getenv("ACG_THOMAS");
+        if (!e) return 0;
+        const std::string s(e);
+        const char* names[] = {"", "2,2,12", "2,4,12", "2,4,8", "4,4,8", "2,8,8", "2,1,12", "4,2,8"};
+        for (int a = 1; a < 8; ++a)
+            if (s == names[a]) return a;
+        return 0;
+    }();
+    return c;
+}
+
+template <typename T, bool Fast, bool Fused>
+void launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
+                   const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
+#define ACG_TH(...) launch_thomas_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, phi_scratch, st)
+    switch (thomas_choice()) {
+        case 1: ACG_TH(ThomasCfg<2, 2, 12>); break;
+        case 2: ACG_TH(ThomasCfg<2, 4, 12>); break;
+        case 3: ACG_TH(ThomasCfg<2, 4, 8>); break;
+        case 4: ACG_TH(ThomasCfg<4, 4, 8>); break;
+        case 5: ACG_TH(ThomasCfg<2, 8, 8>); break;
+        case 6: ACG_TH(ThomasCfg<2, 1, 12>); break;
+        case 7: ACG_TH(ThomasCfg<4, 2, 8>); break;
+        default: ACG_TH(typename ThomasOf<T>::type); break;
+    }
+#undef ACG_TH
+}
+
+}  // namespace
+
+TreePlan make_tree_plan(long long n) {
+    TreePlan p{};
+    p.n = n;
+    int d = 0;
+    while (((n + (1LL << d) - 1) >> d) > 16) ++d;
+    p.depth = d;
+    p.nodes = 1 << d;
+    p.threads = p.nodes < 256 ? p.nodes : 256;
+    p.blocks = p.nodes / p.threads;
+    return p;
+}
+
+size_t thomas_smem_per_block(int dsize, int n_z, bool global_phi) {
+    return dsize == 4 ? thomas_smem_bytes<float, ThomasF32>(n_z, global_phi)
+                      : thomas_smem_bytes<double, ThomasF64>(n_z, global_phi);
+}
+
+template <typename T>
+void launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
+                       T* part_k, Scalars<T>* S, T* phi_scratch, cudaStream_t st) {
+    if (fast)
+        launch_thomas<T, true, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch, st);
+    else
+        launch_thomas<T, false, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch, st);
+    post_launch("fused_prec");
+}
+
+template <typename T>
+void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scalars<T>* S,
+                         const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
+    if (fast)
+        launch_thomas<T, true, false>(v, nullptr, y, x, nullptr, nullptr, S, gate, phi_scratch, st);
+    else
+        launch_thomas<T, false, false>(v, nullptr, y, x, nullptr, nullptr, S, gate, phi_scratch, st);
+    post_launch("precondition");
+}
+
+template <typename T>
+void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
+                       const Scalars<T>* S, cudaStream_t st) {
+    const dim3 block(32, kStencilWarps);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
+    static const bool plain = [] {
+        const char* e = std::getenv("ACG_SPMV");
+        return e && std::string(e) == "plain";
+    }();
+    if (plain) {
+        const size_t smem = sizeof(T) * 4 * static_cast<size_t>(v.n_z);
+        if (fast) {
+            ensure_smem(k_fused_spmv<T, true>, smem);
+            k_fused_spmv<T, true><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+        } else {
+            ensure_smem(k_fused_spmv<T, false>, smem);
+            k_fused_spmv<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+        }
+    } else {
+        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
+                                         static_cast<size_t>(kSpmvD + 1) * 4 * 32 * kStencilWarps);
+        if (fast) {
+            ensure_smem(k_fused_spmv_ring<T, true>, smem);
+            k_fused_spmv_ring<T, true><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+        } else {
+            ensure_smem(k_fused_spmv_ring<T, false>, smem);
+            k_fused_spmv_ring<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+        }
+    }
+    post_launch("fused_spmv");
+}
+
+template <typename T>
+void launch_apply(const SlabView<T>& v, bool fast, const T* x, T* y, const Scalars<T>* gate,
+                  cudaStream_t st) {
+    const dim3 block(32, kStencilWarps);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
+    const size_t smem = sizeof(T) * 4 * static_cast<size_t>(v.n_z);
+    if (fast) {
+        ensure_smem(k_apply<T, true>, smem);
+        k_apply<T, true><<<grid, block, smem, st>>>(v, x, y, gate);
+    } else {
+        ensure_smem(k_apply<T, false>, smem);
+        k_apply<T, false><<<grid, block, smem, st>>>(v, x, y, gate);
+    }
+    post_launch("apply");
+}
+
+template <typename T>
+void launch_residual_partials(const SlabView<T>& v, bool fast, const T* u, const T* f, T* part,
+                              cudaStream_t st) {
+    const dim3 block(32, kStencilWarps);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
+    const size_t smem = sizeof(T) * 4 * static_cast<size_t>(v.n_z);
+    if (fast) {
+        ensure_smem(k_residual_partials<T, true>, smem);
+        k_residual_partials<T, true><<<grid, block, smem, st>>>(v, u, f, part);
+    } else {
+        ensure_smem(k_residual_partials<T, false>, smem);
+        k_residual_partials<T, false><<<grid, block, smem, st>>>(v, u, f, part);
+    }
+    post_launch("residual_partials");
+}
+
+template <typename T>
+void launch_dot_partials(const SlabView<T>& v, const T* x, const T* y, T* part,
+                         const Scalars<T>* gate, cudaStream_t st) {
+    const dim3 block(32, 8);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + 7) / 8);
+    k_dot_partials<T><<<grid, block, 0, st>>>(v, x, y, part, gate);
+    post_launch("dot_partials");
+}
+
+template <typename T>
+void launch_axpy(long long n, T value, const T* coef, bool neg, const T* x, T* y,
+                 const Scalars<T>* gate, cudaStream_t st) {
+    k_axpy<T><<<grid_1d(n, 256), 256, 0, st>>>(n, value, coef, neg ? 1 : 0, x, y, gate);
+    post_launch("axpy");
+}
+
+template <typename T>
+void launch_scal(long long n, T value, const T* coef, T* x, const Scalars<T>* gate,
+                 cudaStream_t st) {
+    k_scal<T><<<grid_1d(n, 256), 256, 0, st>>>(n, value, coef, x, gate);
+    post_launch("scal");
+}
+
+template <typename T>
+void launch_copy(long long n, const T* x, T* y, const Scalars<T>* gate, cudaStream_t st) {
+    k_copy<T><<<grid_1d(n, 256), 256, 0, st>>>(n, x, y, gate);
+    post_launch("copy");
+}
+
+template <typename T>
+void launch_fill(long long n, T value, T* x, cudaStream_t st) {
+    k_fill<T><<<grid_1d(n, 256), 256, 0, st>>>(n, value, x);
+    post_launch("fill");
+}
+
+template <typename T>
+void launch_fill_random(const SlabView<T>& v, uint64_t seed, T* x, cudaStream_t st) {
+    const long long n = static_cast<long long>(v.m_loc) * v.plane;
+    k_fill_random<T><<<grid_1d(n, 256), 256, 0, st>>>(v, seed, x);
+    post_launch("fill_random");
+}
+
+template <typename T>
+void launch_tree_stage1(const TreePlan& plan, const T* in0, const T* in1, const T* in2, int nv,
+                        T* stage, const Scalars<T>* gate, cudaStream_t st) {
+    k_tree1<T><<<plan.blocks, plan.threads, 0, st>>>(plan.n, plan.depth, in0, in1, in2, nv, stage,
+                                                     plan.blocks, gate);
+    post_launch("tree1");
+}
+
+template <typename T>
+void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
+                        bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
+                        cudaStream_t st) {
+    const int nt = plan.blocks < 1024 ? plan.blocks : 1024;
+    k_tree2<T><<<1, nt, 0, st>>>(plan.blocks, stage, nv, gather, slab, finish ? 1 : 0, nslabs,
+                                 exact_tree ? 1 : 0, S, op);
+    post_launch("tree2");
+}
+
+template <typename T>
+void launch_finish(const T* gather, int nv, int nslabs, bool exact_tree, Scalars<T>* S, int op,
+                   cudaStream_t st) {
+    k_finish<T><<<1, 1, 0, st>>>(gather, nv, nslabs, exact_tree ? 1 : 0, S, op);
+    post_launch("finish");
+}
+
+template <typename T>
+void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy, long long isb,
+                      long long osx, long long osb, cudaStream_t st) {
+    const dim3 block(32, 8);
+    const int gz = nb < 65535 ? nb : 65535;
+    const dim3 grid((nx + 31) / 32, (ny + 31) / 32, gz);
+    k_transpose<T><<<grid, block, 0, st>>>(in, out, nx, ny, nb, isy, isb, osx, osb);
+    post_launch("transpose");
+}
+
+#define ACG_INSTANTIATE(T)                                                                      \
+    template void launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,      \
+                                       Scalars<T>*, T*, cudaStream_t);                          \
+    template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
+                                         const Scalars<T>*, T*, cudaStream_t);                  \
+    template void launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,      \
+                                       const Scalars<T>*, cudaStream_t);                        \
+    template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \
+                                  cudaStream_t);                                                \
+    template void launch_residual_partials<T>(const SlabView<T>&, bool, const T*, const T*, T*, \
+                                              cudaStream_t);                                    \
+    template void launch_dot_partials<T>(const SlabView<T>&, const T*, const T*, T*,            \
+                                         const Scalars<T>*, cudaStream_t);                      \
+    template void launch_axpy<T>(long long, T, const T*, bool, const T*, T*, const Scalars<T>*, \
+                                 cudaStream_t);                                                 \
+    template void launch_scal<T>(long long, T, const T*, T*, const Scalars<T>*, cudaStream_t);  \
+    template void launch_copy<T>(long long, const T*, T*, const Scalars<T>*, cudaStream_t);     \
+    template void launch_fill<T>(long long, T, T*, cudaStream_t);                               \
+    template void launch_fill_random<T>(const SlabView<T>&, uint64_t, T*, cudaStream_t);        \
+    template void launch_tree_stage1<T>(const TreePlan&, const T*, const T*, const T*, int, T*, \
+                                        const Scalars<T>*, cudaStream_t);                       \
+    template void launch_tree_stage2<T>(const TreePlan&, const T*, int, T*, int, bool, int,     \
+                                        bool, Scalars<T>*, int, cudaStream_t);                  \
+    template void launch_finish<T>(const T*, int, int, bool, Scalars<T>*, int, cudaStream_t);   \
+    template void launch_transpose<T>(const T*, T*, int, int, int, long long, long long,        \
+                                      long long, long long, cudaStream_t);
+
+ACG_INSTANTIATE(double)
+ACG_INSTANTIATE(float)
+
+}  // namespace acg

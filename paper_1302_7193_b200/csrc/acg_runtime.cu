@@ -1,0 +1,1563 @@
+// Host runtime of libacg_cuda.so: the C ABI of include/acg.h.
+//
+// Owns device contexts (profile + per-column geometry per i-slab), fields,
+// halo exchange between slabs (device copies on one GPU, NCCL send/recv
+// across processes), the exact pairwise reductions, and the device-resident
+// PCG drivers (solver.hpp:162-370) whose scalar recurrences run on the GPU so
+// the loop never waits on the host.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only; NCCL itself is dlopen'ed on first use
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/acg.h"
+#include "acg_internal.h"
+
+using namespace acg;
+
+// =================================================================== errors
+namespace {
+
+thread_local std::string t_err;
+
+struct Fail {
+    acg_status st;
+};
+
+[[noreturn]] void fail(acg_status st, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    throw Fail{st};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ACG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call) cuda_check((call), #call)
+
+template <typename F>
+acg_status guarded(F&& f) {
+    try {
+        f();
+        return ACG_OK;
+    } catch (const Fail& e) {
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        t_err = "out of host memory";
+        return ACG_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return ACG_ERR_INTERNAL;
+    }
+}
+
+// ===================================================================== NCCL
+struct NcclApi {
+    void* h = nullptr;
+    decltype(&::ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&::ncclCommInitRank) commInitRank = nullptr;
+    decltype(&::ncclCommDestroy) commDestroy = nullptr;
+    decltype(&::ncclCommAbort) commAbort = nullptr;
+    decltype(&::ncclGetErrorString) errorString = nullptr;
+    decltype(&::ncclAllGather) allGather = nullptr;
+    decltype(&::ncclSend) send = nullptr;
+    decltype(&::ncclRecv) recv = nullptr;
+    decltype(&::ncclGroupStart) groupStart = nullptr;
+    decltype(&::ncclGroupEnd) groupEnd = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names) {
+            api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (api.h) break;
+        }
+        if (!api.h) return;
+#define ACG_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(api.h, name))
+        ACG_SYM(getUniqueId, "ncclGetUniqueId");
+        ACG_SYM(commInitRank, "ncclCommInitRank");
+        ACG_SYM(commDestroy, "ncclCommDestroy");
+        ACG_SYM(commAbort, "ncclCommAbort");
+        ACG_SYM(errorString, "ncclGetErrorString");
+        ACG_SYM(allGather, "ncclAllGather");
+        ACG_SYM(send, "ncclSend");
+        ACG_SYM(recv, "ncclRecv");
+        ACG_SYM(groupStart, "ncclGroupStart");
+        ACG_SYM(groupEnd, "ncclGroupEnd");
+#undef ACG_SYM
+    });
+    if (!api.h || !api.getUniqueId || !api.commInitRank || !api.allGather || !api.send)
+        fail(ACG_ERR_NCCL, "NCCL runtime (libnccl.so.2) could not be loaded");
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(ACG_ERR_NCCL, "%s: %s", what, nccl().errorString ? nccl().errorString(r) : "error");
+}
+
+}  // namespace
+
+struct acg_comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1, device = 0;
+};
+
+// ================================================================== context
+namespace {
+
+struct Slab {
+    int index = 0;  // global slab index
+    int i0 = 0, i1 = 0, m_loc = 0;
+    long long plane = 0, n_loc = 0;
+    void* prof = nullptr;
+    void* col = nullptr;
+    void* part[3] = {nullptr, nullptr, nullptr};
+    void* stage = nullptr;
+    void* phi = nullptr;
+    void* staging = nullptr;
+    void* tmp = nullptr;  // Scalars<T> for API calls
+    TreePlan plan{};
+};
+
+size_t dsize(acg_dtype t) { return t == ACG_F32 ? sizeof(float) : sizeof(double); }
+
+bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// Node [lo, hi) of the reference's pairwise tree (parallel.hpp:11-20) at `depth`.
+void tree_node(long long n, int depth, long long t, long long& lo, long long& hi) {
+    lo = 0;
+    hi = n;
+    for (int b = depth - 1; b >= 0; --b) {
+        const long long mid = lo + (hi - lo) / 2;
+        if ((t >> b) & 1)
+            lo = mid;
+        else
+            hi = mid;
+    }
+}
+
+}  // namespace
+
+struct acg_context {
+    acg_dtype dtype = ACG_F64;
+    acg_math math = ACG_MATH_EXACT;
+    int m = 0, n_z = 0, device = 0;
+    int nslabs_total = 1, rank = 0;
+    acg_comm* comm = nullptr;
+    cudaStream_t stream = nullptr;
+    bool exact_tree = true;
+    std::vector<Slab> slabs;  // local slabs (same device)
+    void* gather = nullptr;       // nslabs_total * 4 T
+    void* gather_send = nullptr;  // 4 T (NCCL)
+    std::vector<acg_field*> pool; // reusable scratch fields (host entry points)
+    size_t s = 8;
+    bool fast() const { return math == ACG_MATH_FAST; }
+};
+
+struct acg_field {
+    const acg_context* ctx = nullptr;
+    std::vector<void*> base;  // per local slab: (m_loc + 2) planes
+    void* data(size_t i) const {
+        return static_cast<char*>(base[i]) + ctx->slabs[i].plane * ctx->s;
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+SlabView<T> view(const acg_context* c, size_t si) {
+    const Slab& s = c->slabs[si];
+    SlabView<T> v;
+    v.m = c->m;
+    v.n_z = c->n_z;
+    v.m_loc = s.m_loc;
+    v.i0 = s.i0;
+    v.plane = s.plane;
+    v.prof = static_cast<const T*>(s.prof);
+    v.col = static_cast<const T*>(s.col);
+    return v;
+}
+
+void check_ctx(const acg_context* c) {
+    if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "null context");
+}
+void check_field(const acg_context* c, const acg_field* f, const char* what) {
+    if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "%s: null field", what);
+    if (f->ctx != c && !(f->ctx && c && f->ctx->m == c->m && f->ctx->n_z == c->n_z &&
+                         f->ctx->slabs.size() == c->slabs.size() && f->ctx->dtype == c->dtype))
+        fail(ACG_ERR_INVALID_ARGUMENT, "%s: field does not match operator context", what);
+}
+
+template <typename T>
+void build_slab_tables(const acg_context* c, Slab& s, const acg_operator_desc* d) {
+    const int m = c->m, n_z = c->n_z;
+    std::vector<T> prof(static_cast<size_t>(kProfRows) * n_z);
+    for (int k = 0; k < n_z; ++k) {
+        // OperatorContext<T> converts each double to T (operator.hpp:36-43); the
+        // per-level combination (a'-b')-c' is then formed in T exactly as the
+        // kernels of operator.hpp:127/:307 form it.
+        const T a = static_cast<T>(d->a_prime[k]), b = static_cast<T>(d->b_prime[k]);
+        const T cc = static_cast<T>(d->c_prime[k]), dd = static_cast<T>(d->d[k]);
+        volatile T ab = a - b;  // keep the two roundings separate
+        prof[kProfS * n_z + k] = static_cast<T>(ab) - cc;
+        prof[kProfB * n_z + k] = b;
+        prof[kProfC * n_z + k] = cc;
+        prof[kProfD * n_z + k] = dd;
+        prof[kProfInvD * n_z + k] = T(1) / dd;
+    }
+    const long long ncol = static_cast<long long>(s.m_loc) * m;
+    std::vector<T> col(static_cast<size_t>(kColRows) * ncol);
+    for (int il = 0; il < s.m_loc; ++il) {
+        const int i = s.i0 + il;
+        for (int j = 0; j < m; ++j) {
+            const long long ci = static_cast<long long>(il) * m + j;
+            const size_t g = static_cast<size_t>(i) * m + j;
+            const T area = static_cast<T>(d->cell_area[g]);
+            const T adiag = static_cast<T>(d->alpha_diag[g]);
+            col[kColArea * ncol + ci] = area;
+            col[kColDiag * ncol + ci] = adiag;
+            col[kColAtil * ncol + ci] = adiag / area;
+            col[kColE * ncol + ci] =
+                i + 1 < m ? static_cast<T>(d->alpha_east[static_cast<size_t>(i) * m + j]) : T(0);
+            col[kColW * ncol + ci] =
+                i > 0 ? static_cast<T>(d->alpha_east[static_cast<size_t>(i - 1) * m + j]) : T(0);
+            col[kColN * ncol + ci] =
+                j + 1 < m ? static_cast<T>(d->alpha_north[static_cast<size_t>(i) * (m - 1) + j])
+                          : T(0);
+            col[kColS * ncol + ci] =
+                j > 0 ? static_cast<T>(d->alpha_north[static_cast<size_t>(i) * (m - 1) + j - 1])
+                      : T(0);
+            col[kColInvA * ncol + ci] = T(1) / area;
+        }
+    }
+    CK(cudaMalloc(&s.prof, prof.size() * sizeof(T)));
+    CK(cudaMemcpy(s.prof, prof.data(), prof.size() * sizeof(T), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&s.col, col.size() * sizeof(T)));
+    CK(cudaMemcpy(s.col, col.data(), col.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+void free_slab(Slab& s) {
+    void* ps[] = {s.prof, s.col, s.part[0], s.part[1], s.part[2], s.stage, s.phi, s.staging, s.tmp};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    s = Slab{};
+}
+
+// Partition of the m i-planes into p contiguous slabs. When p is a power of
+// two and the depth-log2(p) nodes of the reference's column-order pairwise
+// tree fall on plane boundaries, those nodes ARE the slabs: every slab then
+// sums a complete subtree and the perfect tree above reproduces the CPU sum
+// bit for bit.
+void partition(int m, int p, std::vector<std::pair<int, int>>& out, bool& exact) {
+    out.clear();
+    const long long n = static_cast<long long>(m) * m;
+    exact = (p == 1);
+    if (p > 1 && is_pow2(p)) {
+        int depth = 0;
+        while ((1 << depth) < p) ++depth;
+        bool ok = (n >> (depth - 1)) > 8;  // every node above the slabs is a split node
+        std::vector<std::pair<int, int>> cand;
+        for (int r = 0; r < p && ok; ++r) {
+            long long lo, hi;
+            tree_node(n, depth, r, lo, hi);
+            if (lo % m || hi % m || hi <= lo) ok = false;
+            cand.emplace_back(static_cast<int>(lo / m), static_cast<int>(hi / m));
+        }
+        if (ok) {
+            out = cand;
+            exact = true;
+            return;
+        }
+    }
+    for (int r = 0; r < p; ++r)
+        out.emplace_back(static_cast<int>(static_cast<long long>(r) * m / p),
+                         static_cast<int>(static_cast<long long>(r + 1) * m / p));
+}
+
+template <typename T>
+void* alloc_tmp_scalars() {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(Scalars<T>)));
+    CK(cudaMemset(p, 0, sizeof(Scalars<T>)));
+    return p;
+}
+
+}  // namespace
+
+// =================================================================== basics
+extern "C" {
+
+const char* acg_last_error(void) { return t_err.c_str(); }
+int acg_abi_version(void) { return ACG_ABI_VERSION; }
+long long acg_kernel_launch_count(void) { return g_launches; }
+
+acg_status acg_device_count(int* count) {
+    return guarded([&] {
+        if (!count) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        CK(cudaGetDeviceCount(count));
+    });
+}
+
+acg_status acg_host_alloc(void** ptr, size_t bytes) {
+    return guarded([&] {
+        if (!ptr) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        CK(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable));
+    });
+}
+
+acg_status acg_host_free(void* ptr) {
+    return guarded([&] {
+        if (ptr) CK(cudaFreeHost(ptr));
+    });
+}
+
+acg_status acg_comm_unique_id(void* id128) {
+    return guarded([&] {
+        if (!id128) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        ncclUniqueId id;
+        nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(id128, &id, sizeof(id));
+    });
+}
+
+acg_status acg_comm_create(acg_comm** out, int rank, int nranks, const void* id128, int device) {
+    return guarded([&] {
+        if (!out || !id128) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            fail(ACG_ERR_INVALID_ARGUMENT, "bad rank %d of %d", rank, nranks);
+        DeviceGuard g(device);
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        auto c = std::make_unique<acg_comm>();
+        c->rank = rank;
+        c->nranks = nranks;
+        c->device = device;
+        nccl_check(nccl().commInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+        *out = c.release();
+    });
+}
+
+acg_status acg_comm_destroy(acg_comm* c) {
+    return guarded([&] {
+        if (!c) return;
+        if (c->comm) nccl().commDestroy(c->comm);
+        delete c;
+    });
+}
+
+acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_operator_desc* d,
+                              const acg_placement* pl) {
+    return guarded([&] {
+        if (!out || !d) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        if (d->m < 1 || d->n_z < 1)
+            fail(ACG_ERR_INVALID_ARGUMENT, "OperatorContext: empty profile or geometry");
+        if (dtype != ACG_F64 && dtype != ACG_F32) fail(ACG_ERR_INVALID_ARGUMENT, "bad dtype");
+        if (!d->a_prime || !d->b_prime || !d->c_prime || !d->d || !d->cell_area || !d->alpha_diag ||
+            (d->m > 1 && (!d->alpha_east || !d->alpha_north)))
+            fail(ACG_ERR_INVALID_ARGUMENT, "OperatorContext: missing coefficient array");
+        auto c = std::make_unique<acg_context>();
+        c->dtype = dtype;
+        c->s = dsize(dtype);
+        c->m = d->m;
+        c->n_z = d->n_z;
+        int p = 1;
+        if (pl) {
+            c->math = pl->math;
+            c->device = pl->device;
+            c->comm = pl->comm;
+            if (pl->comm) {
+                p = pl->comm->nranks;
+                c->rank = pl->comm->rank;
+                if (pl->comm->device != pl->device)
+                    fail(ACG_ERR_INVALID_ARGUMENT, "placement device differs from comm device");
+            } else {
+                p = pl->slabs < 1 ? 1 : pl->slabs;
+            }
+        } else {
+            cudaGetDevice(&c->device);
+        }
+        if (p > d->m) fail(ACG_ERR_INVALID_ARGUMENT, "more slabs (%d) than i-planes (%d)", p, d->m);
+        if (p > 64) fail(ACG_ERR_INVALID_ARGUMENT, "at most 64 slabs are supported");
+        c->nslabs_total = p;
+        DeviceGuard g(c->device);
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        std::vector<std::pair<int, int>> parts;
+        partition(d->m, p, parts, c->exact_tree);
+        std::vector<int> mine;
+        if (c->comm)
+            mine.push_back(c->rank);
+        else
+            for (int r = 0; r < p; ++r) mine.push_back(r);
+        c->slabs.resize(mine.size());
+        for (size_t a = 0; a < mine.size(); ++a) {
+            Slab& s = c->slabs[a];
+            s.index = mine[a];
+            s.i0 = parts[mine[a]].first;
+            s.i1 = parts[mine[a]].second;
+            s.m_loc = s.i1 - s.i0;
+            s.plane = static_cast<long long>(d->n_z) * d->m;
+            s.n_loc = s.plane * s.m_loc;
+            if (dtype == ACG_F32) {
+                build_slab_tables<float>(c.get(), s, d);
+                s.tmp = alloc_tmp_scalars<float>();
+            } else {
+                build_slab_tables<double>(c.get(), s, d);
+                s.tmp = alloc_tmp_scalars<double>();
+            }
+            const long long ncol = static_cast<long long>(s.m_loc) * d->m;
+            for (int a2 = 0; a2 < 3; ++a2) CK(cudaMalloc(&s.part[a2], ncol * c->s));
+            s.plan = make_tree_plan(ncol);
+            if (s.plan.blocks > 16384)
+                fail(ACG_ERR_INVALID_ARGUMENT, "slab of %lld columns exceeds the reduction plan",
+                     ncol);
+            CK(cudaMalloc(&s.stage, 3 * static_cast<size_t>(s.plan.blocks) * c->s));
+            if (thomas_smem_per_block(static_cast<int>(c->s), d->n_z, false) > 200 * 1024)
+                CK(cudaMalloc(&s.phi, s.n_loc * c->s));  // tall columns: phi in HBM
+        }
+        CK(cudaMalloc(&c->gather, static_cast<size_t>(p) * 4 * c->s));
+        CK(cudaMemset(c->gather, 0, static_cast<size_t>(p) * 4 * c->s));
+        CK(cudaMalloc(&c->gather_send, 4 * c->s));
+        *out = c.release();
+    });
+}
+
+acg_status acg_context_destroy(acg_context* c) {
+    return guarded([&] {
+        if (!c) return;
+        DeviceGuard g(c->device);
+        cudaStreamSynchronize(c->stream);
+        for (acg_field* f : c->pool) {
+            for (void* b : f->base) cudaFree(b);
+            delete f;
+        }
+        for (Slab& s : c->slabs) free_slab(s);
+        if (c->gather) cudaFree(c->gather);
+        if (c->gather_send) cudaFree(c->gather_send);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+acg_status acg_context_info_get(const acg_context* c, acg_context_info* o) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!o) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        o->m = c->m;
+        o->n_z = c->n_z;
+        o->dtype = c->dtype;
+        o->math = c->math;
+        o->nslabs_total = c->nslabs_total;
+        o->nslabs_local = static_cast<int>(c->slabs.size());
+        o->rank = c->rank;
+        o->i_begin = c->slabs.front().i0;
+        o->i_end = c->slabs.back().i1;
+        o->exact_tree = c->exact_tree ? 1 : 0;
+        size_t b = 0;
+        for (const Slab& s : c->slabs) b += static_cast<size_t>(s.n_loc) * c->s;
+        o->bytes_per_field_local = b;
+    });
+}
+
+acg_status acg_synchronize(const acg_context* c) {
+    return guarded([&] {
+        check_ctx(c);
+        DeviceGuard g(c->device);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+void* acg_context_stream(const acg_context* c) { return c ? c->stream : nullptr; }
+
+}  // extern "C"
+
+// ==================================================================== fields
+namespace {
+
+acg_field* new_field(const acg_context* c) {
+    auto f = std::make_unique<acg_field>();
+    f->ctx = c;
+    for (const Slab& s : c->slabs) {
+        void* p = nullptr;
+        const size_t bytes = static_cast<size_t>(s.n_loc + 2 * s.plane) * c->s;
+        CK(cudaMalloc(&p, bytes));
+        f->base.push_back(p);
+        CK(cudaMemsetAsync(p, 0, bytes, c->stream));
+    }
+    return f.release();
+}
+
+void free_field(acg_field* f) {
+    for (void* b : f->base) cudaFree(b);
+    delete f;
+}
+
+struct PoolField {
+    acg_context* c;
+    acg_field* f;
+    explicit PoolField(const acg_context* cc) : c(const_cast<acg_context*>(cc)) {
+        if (!c->pool.empty()) {
+            f = c->pool.back();
+            c->pool.pop_back();
+        } else {
+            f = new_field(c);
+        }
+    }
+    ~PoolField() { c->pool.push_back(f); }
+};
+
+void* staging(const acg_context* c, size_t si) {
+    Slab& s = const_cast<Slab&>(c->slabs[si]);
+    if (!s.staging) CK(cudaMalloc(&s.staging, static_cast<size_t>(s.n_loc) * c->s));
+    return s.staging;
+}
+
+template <typename T>
+void upload_t(acg_field* f, const void* host, acg_layout layout, acg_host_scope scope) {
+    const acg_context* c = f->ctx;
+    const int m = c->m, n_z = c->n_z;
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        T* st = static_cast<T*>(staging(c, si));
+        T* dst = static_cast<T*>(f->data(si));
+        if (layout == ACG_LAYOUT_VERTICAL) {
+            const T* src = static_cast<const T*>(host) +
+                           (scope == ACG_HOST_FULL ? static_cast<size_t>(s.i0) * m * n_z : 0);
+            CK(cudaMemcpyAsync(st, src, static_cast<size_t>(s.n_loc) * sizeof(T),
+                               cudaMemcpyHostToDevice, c->stream));
+            // st[(il*m + j)*n_z + k] -> dst[il*plane + k*m + j]
+            launch_transpose<T>(st, dst, n_z, m, s.m_loc, n_z, static_cast<long long>(m) * n_z, m,
+                                s.plane, c->stream);
+        } else {
+            if (scope == ACG_HOST_FULL) {
+                CK(cudaMemcpy2DAsync(st, s.m_loc * sizeof(T),
+                                     static_cast<const T*>(host) + s.i0, m * sizeof(T),
+                                     s.m_loc * sizeof(T), static_cast<size_t>(m) * n_z,
+                                     cudaMemcpyHostToDevice, c->stream));
+            } else {
+                CK(cudaMemcpyAsync(st, host, static_cast<size_t>(s.n_loc) * sizeof(T),
+                                   cudaMemcpyHostToDevice, c->stream));
+            }
+            // st[(j*n_z + k)*m_loc + il] -> dst[il*plane + k*m + j]
+            launch_transpose<T>(st, dst, s.m_loc, m, n_z, static_cast<long long>(n_z) * s.m_loc,
+                                s.m_loc, s.plane, m, c->stream);
+        }
+        CK(cudaPeekAtLastError());
+    }
+}
+
+template <typename T>
+void download_t(const acg_field* f, void* host, acg_layout layout, acg_host_scope scope) {
+    const acg_context* c = f->ctx;
+    const int m = c->m, n_z = c->n_z;
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        T* st = static_cast<T*>(staging(c, si));
+        const T* src = static_cast<const T*>(f->data(si));
+        if (layout == ACG_LAYOUT_VERTICAL) {
+            // src[il*plane + k*m + j] -> st[(il*m + j)*n_z + k]
+            launch_transpose<T>(src, st, m, n_z, s.m_loc, m, s.plane, n_z,
+                                static_cast<long long>(m) * n_z, c->stream);
+            T* dst = static_cast<T*>(host) +
+                     (scope == ACG_HOST_FULL ? static_cast<size_t>(s.i0) * m * n_z : 0);
+            CK(cudaMemcpyAsync(dst, st, static_cast<size_t>(s.n_loc) * sizeof(T),
+                               cudaMemcpyDeviceToHost, c->stream));
+        } else {
+            // src[il*plane + k*m + j] -> st[(j*n_z + k)*m_loc + il]
+            launch_transpose<T>(src, st, m, s.m_loc, n_z, s.plane, m,
+                                static_cast<long long>(n_z) * s.m_loc, s.m_loc, c->stream);
+            if (scope == ACG_HOST_FULL) {
+                CK(cudaMemcpy2DAsync(static_cast<T*>(host) + s.i0, m * sizeof(T), st,
+                                     s.m_loc * sizeof(T), s.m_loc * sizeof(T),
+                                     static_cast<size_t>(m) * n_z, cudaMemcpyDeviceToHost,
+                                     c->stream));
+            } else {
+                CK(cudaMemcpyAsync(host, st, static_cast<size_t>(s.n_loc) * sizeof(T),
+                                   cudaMemcpyDeviceToHost, c->stream));
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+// ---------------------------------------------------------------- halos
+// Ghost plane -1 of slab s <- plane m_loc-1 of slab s-1; ghost plane m_loc of
+// slab s <- plane 0 of slab s+1. Device copies between local slabs, NCCL
+// send/recv between ranks.
+void halo(const acg_context* c, const acg_field* f) {
+    if (c->nslabs_total == 1) return;
+    const size_t pb = static_cast<size_t>(c->slabs[0].plane) * c->s;
+    auto plane_ptr = [&](size_t si, int il) {
+        return static_cast<char*>(f->base[si]) + static_cast<size_t>(il + 1) * pb;
+    };
+    if (!c->comm) {
+        for (size_t si = 1; si < c->slabs.size(); ++si) {
+            const Slab& lo = c->slabs[si - 1];
+            const Slab& hi = c->slabs[si];
+            CK(cudaMemcpyAsync(plane_ptr(si, -1), plane_ptr(si - 1, lo.m_loc - 1), pb,
+                               cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(plane_ptr(si - 1, lo.m_loc), plane_ptr(si, 0), pb,
+                               cudaMemcpyDeviceToDevice, c->stream));
+            (void)hi;
+        }
+        return;
+    }
+    NcclApi& api = nccl();
+    const int r = c->rank, p = c->nslabs_total;
+    const Slab& s = c->slabs[0];
+    const ncclDataType_t dt = c->dtype == ACG_F32 ? ncclFloat32 : ncclFloat64;
+    const size_t cnt = static_cast<size_t>(s.plane);
+    nccl_check(api.groupStart(), "ncclGroupStart");
+    if (r > 0) {
+        nccl_check(api.send(plane_ptr(0, 0), cnt, dt, r - 1, c->comm->comm, c->stream), "ncclSend");
+        nccl_check(api.recv(plane_ptr(0, -1), cnt, dt, r - 1, c->comm->comm, c->stream), "ncclRecv");
+    }
+    if (r + 1 < p) {
+        nccl_check(api.send(plane_ptr(0, s.m_loc - 1), cnt, dt, r + 1, c->comm->comm, c->stream),
+                   "ncclSend");
+        nccl_check(api.recv(plane_ptr(0, s.m_loc), cnt, dt, r + 1, c->comm->comm, c->stream),
+                   "ncclRecv");
+    }
+    nccl_check(api.groupEnd(), "ncclGroupEnd");
+}
+
+// -------------------------------------------------------------- reductions
+// Reduce nv per-column partial arrays of every local slab (already written to
+// slab.part[0..nv)) and run scalar program `op` on every slab's Scalars.
+template <typename T>
+void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>& S,
+            const Scalars<T>* gate_or_null, bool gated) {
+    const bool single = c->nslabs_total == 1;
+    T* gather = static_cast<T*>(c->gather);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        const Scalars<T>* gate = gated ? (gate_or_null ? gate_or_null : S[si]) : nullptr;
+        launch_tree_stage1<T>(s.plan, static_cast<const T*>(s.part[0]),
+                              static_cast<const T*>(s.part[1]), static_cast<const T*>(s.part[2]),
+                              nv, static_cast<T*>(s.stage), gate, c->stream);
+        T* g = c->comm ? static_cast<T*>(c->gather_send) : gather;
+        const int slot = c->comm ? 0 : s.index;
+        launch_tree_stage2<T>(s.plan, static_cast<const T*>(s.stage), nv, g, slot, single,
+                              c->nslabs_total, c->exact_tree, S[si], op, c->stream);
+    }
+    if (single) return;
+    if (c->comm) {
+        const ncclDataType_t dt = c->dtype == ACG_F32 ? ncclFloat32 : ncclFloat64;
+        nccl_check(nccl().allGather(c->gather_send, c->gather, 4, dt, c->comm->comm, c->stream),
+                   "ncclAllGather");
+    }
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_finish<T>(gather, nv, c->nslabs_total, c->exact_tree, S[si], op, c->stream);
+}
+
+template <typename T>
+std::vector<Scalars<T>*> tmp_scalars(const acg_context* c) {
+    std::vector<Scalars<T>*> v;
+    for (const Slab& s : c->slabs) v.push_back(static_cast<Scalars<T>*>(s.tmp));
+    return v;
+}
+
+template <typename T>
+Scalars<T> read_scalars(const acg_context* c, const Scalars<T>* dev) {
+    Scalars<T> h;
+    CK(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return h;
+}
+
+template <typename T>
+void reset_tmp(const acg_context* c, T alpha = T(0), T beta = T(0)) {
+    Scalars<T> h{};
+    h.alpha = alpha;
+    h.beta = beta;
+    for (const Slab& s : c->slabs)
+        CK(cudaMemcpyAsync(s.tmp, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+}
+
+// ------------------------------------------------------------ device ops
+template <typename T>
+void op_apply(const acg_context* c, const acg_field* x, acg_field* y, const Scalars<T>* gate) {
+    halo(c, x);
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_apply<T>(view<T>(c, si), c->fast(), static_cast<const T*>(x->data(si)),
+                        static_cast<T*>(y->data(si)), gate, c->stream);
+}
+
+template <typename T>
+void op_precondition(const acg_context* c, const acg_field* y, acg_field* x,
+                     const std::vector<Scalars<T>*>& flag, const Scalars<T>* gate) {
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_precondition<T>(view<T>(c, si), c->fast(), static_cast<const T*>(y->data(si)),
+                               static_cast<T*>(x->data(si)), flag[si], gate,
+                               static_cast<T*>(c->slabs[si].phi), c->stream);
+}
+
+template <typename T>
+void op_dot(const acg_context* c, const acg_field* x, const acg_field* y, int op,
+            const std::vector<Scalars<T>*>& S, bool gated) {
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_dot_partials<T>(view<T>(c, si), static_cast<const T*>(x->data(si)),
+                               static_cast<const T*>(y->data(si)),
+                               static_cast<T*>(c->slabs[si].part[0]), gated ? S[si] : nullptr,
+                               c->stream);
+    reduce<T>(c, 1, op, S, nullptr, gated);
+}
+
+template <typename T>
+void op_axpy(const acg_context* c, T value, const std::vector<Scalars<T>*>* coefS, int which,
+             bool neg, const acg_field* x, acg_field* y, bool gated) {
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const T* coef = nullptr;
+        const Scalars<T>* g = nullptr;
+        if (coefS) {
+            Scalars<T>* S = (*coefS)[si];
+            coef = which == 0 ? &S->alpha : (which == 1 ? &S->beta : nullptr);
+            if (gated) g = S;  // gated on the solver's done flag
+        }
+        launch_axpy<T>(c->slabs[si].n_loc, value, coef, neg, static_cast<const T*>(x->data(si)),
+                       static_cast<T*>(y->data(si)), g, c->stream);
+    }
+}
+
+template <typename T>
+void op_copy(const acg_context* c, const acg_field* x, acg_field* y, const std::vector<Scalars<T>*>* gS) {
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_copy<T>(c->slabs[si].n_loc, static_cast<const T*>(x->data(si)),
+                       static_cast<T*>(y->data(si)), gS ? (*gS)[si] : nullptr, c->stream);
+}
+
+template <typename T>
+T op_true_residual(const acg_context* c, const acg_field* u, const acg_field* f) {
+    halo(c, u);
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_residual_partials<T>(view<T>(c, si), c->fast(), static_cast<const T*>(u->data(si)),
+                                    static_cast<const T*>(f->data(si)),
+                                    static_cast<T*>(c->slabs[si].part[0]), c->stream);
+    auto S = tmp_scalars<T>(c);
+    reset_tmp<T>(c);
+    reduce<T>(c, 1, kOpStore, S, nullptr, false);
+    const Scalars<T> h = read_scalars<T>(c, S[0]);
+    return std::sqrt(h.val[0]);  // nrm2's sqrt in T (field.hpp:172)
+}
+
+void check_same(const acg_field* a, const acg_field* b, const char* what) {
+    if (!a || !b) fail(ACG_ERR_INVALID_ARGUMENT, "%s: null field", what);
+    if (a->ctx->m != b->ctx->m || a->ctx->n_z != b->ctx->n_z || a->ctx->dtype != b->ctx->dtype ||
+        a->ctx->slabs.size() != b->ctx->slabs.size())
+        fail(ACG_ERR_INVALID_ARGUMENT, "%s: shape/layout mismatch", what);
+}
+
+#define ACG_TDISPATCH(ctx, ...)          \
+    do {                                 \
+        if ((ctx)->dtype == ACG_F32) {   \
+            using T = float;             \
+            __VA_ARGS__;                 \
+        } else {                         \
+            using T = double;            \
+            __VA_ARGS__;                 \
+        }                                \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+acg_status acg_field_create(acg_field** out, const acg_context* c) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        DeviceGuard g(c->device);
+        *out = new_field(c);
+    });
+}
+
+acg_status acg_field_destroy(acg_field* f) {
+    return guarded([&] {
+        if (!f) return;
+        DeviceGuard g(f->ctx->device);
+        cudaStreamSynchronize(f->ctx->stream);
+        free_field(f);
+    });
+}
+
+acg_status acg_field_upload(acg_field* f, const void* host, acg_layout layout,
+                            acg_host_scope scope) {
+    return guarded([&] {
+        if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = f->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, upload_t<T>(f, host, layout, scope));
+    });
+}
+
+acg_status acg_field_download(const acg_field* f, void* host, acg_layout layout,
+                              acg_host_scope scope) {
+    return guarded([&] {
+        if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = f->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, download_t<T>(f, host, layout, scope));
+    });
+}
+
+acg_status acg_field_fill(acg_field* f, double value) {
+    return guarded([&] {
+        if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
+        const acg_context* c = f->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            for (size_t si = 0; si < c->slabs.size(); ++si)
+                launch_fill<T>(c->slabs[si].n_loc, static_cast<T>(value),
+                               static_cast<T*>(f->data(si)), c->stream);
+        });
+        CK(cudaPeekAtLastError());
+    });
+}
+
+acg_status acg_field_fill_random(acg_field* f, uint64_t seed) {
+    return guarded([&] {
+        if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
+        const acg_context* c = f->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            for (size_t si = 0; si < c->slabs.size(); ++si)
+                launch_fill_random<T>(view<T>(c, si), seed, static_cast<T*>(f->data(si)),
+                                      c->stream);
+        });
+        CK(cudaPeekAtLastError());
+    });
+}
+
+acg_status acg_field_copy(acg_field* dst, const acg_field* src) {
+    return guarded([&] {
+        check_same(dst, src, "copy");
+        const acg_context* c = dst->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, op_copy<T>(c, src, dst, nullptr));
+        CK(cudaPeekAtLastError());
+    });
+}
+
+acg_status acg_apply(const acg_context* c, const acg_field* x, acg_field* y) {
+    return guarded([&] {
+        check_ctx(c);
+        check_field(c, x, "apply");
+        check_field(c, y, "apply");
+        if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "apply: x and y must not alias");
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, op_apply<T>(c, x, y, nullptr));
+        CK(cudaPeekAtLastError());
+    });
+}
+
+acg_status acg_precondition(const acg_context* c, const acg_field* y, acg_field* x) {
+    return guarded([&] {
+        check_ctx(c);
+        check_field(c, y, "precondition");
+        check_field(c, x, "precondition");
+        if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "precondition: y and x must not alias");
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            reset_tmp<T>(c);
+            auto S = tmp_scalars<T>(c);
+            op_precondition<T>(c, y, x, S, nullptr);
+            CK(cudaPeekAtLastError());
+            for (Scalars<T>* s : S)
+                if (read_scalars<T>(c, s).pivot)
+                    fail(ACG_ERR_BREAKDOWN, "precondition: zero pivot in tridiagonal elimination");
+        });
+    });
+}
+
+acg_status acg_axpy(double alpha, const acg_field* x, acg_field* y) {
+    return guarded([&] {
+        check_same(x, y, "axpy");
+        const acg_context* c = x->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, op_axpy<T>(c, static_cast<T>(alpha), nullptr, -1, false, x, y, false));
+        CK(cudaPeekAtLastError());
+    });
+}
+
+acg_status acg_scal(double alpha, acg_field* x) {
+    return guarded([&] {
+        if (!x) fail(ACG_ERR_INVALID_ARGUMENT, "scal: null field");
+        const acg_context* c = x->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            for (size_t si = 0; si < c->slabs.size(); ++si)
+                launch_scal<T>(c->slabs[si].n_loc, static_cast<T>(alpha), nullptr,
+                               static_cast<T*>(x->data(si)), nullptr, c->stream);
+        });
+        CK(cudaPeekAtLastError());
+    });
+}
+
+acg_status acg_dot(const acg_field* x, const acg_field* y, double* out) {
+    return guarded([&] {
+        check_same(x, y, "dot");
+        if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        const acg_context* c = x->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            reset_tmp<T>(c);
+            auto S = tmp_scalars<T>(c);
+            op_dot<T>(c, x, y, kOpStore, S, false);
+            *out = static_cast<double>(read_scalars<T>(c, S[0]).val[0]);
+        });
+    });
+}
+
+acg_status acg_nrm2(const acg_field* x, double* out) {
+    return guarded([&] {
+        if (!x || !out) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = x->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            reset_tmp<T>(c);
+            auto S = tmp_scalars<T>(c);
+            op_dot<T>(c, x, x, kOpStore, S, false);
+            *out = static_cast<double>(std::sqrt(read_scalars<T>(c, S[0]).val[0]));
+        });
+    });
+}
+
+acg_status acg_true_residual(const acg_context* c, const acg_field* u, const acg_field* f,
+                             double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        check_field(c, u, "true_residual");
+        check_field(c, f, "true_residual");
+        if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, *out = static_cast<double>(op_true_residual<T>(c, u, f)));
+    });
+}
+
+acg_status acg_interleaved_spmv_kernel(const acg_context* c, acg_field* u, acg_field* p,
+                                       acg_field* q, const acg_field* z, double alpha,
+                                       double beta, double* sigma) {
+    return guarded([&] {
+        check_ctx(c);
+        for (const acg_field* f : {static_cast<const acg_field*>(u), static_cast<const acg_field*>(p),
+                                   static_cast<const acg_field*>(q), z})
+            check_field(c, f, "interleaved_spmv_kernel");
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            reset_tmp<T>(c, static_cast<T>(alpha), static_cast<T>(beta));
+            auto S = tmp_scalars<T>(c);
+            halo(c, z);
+            for (size_t si = 0; si < c->slabs.size(); ++si)
+                launch_fused_spmv<T>(view<T>(c, si), c->fast(), static_cast<T*>(u->data(si)),
+                                     static_cast<T*>(p->data(si)), static_cast<T*>(q->data(si)),
+                                     static_cast<const T*>(z->data(si)),
+                                     static_cast<T*>(c->slabs[si].part[0]), S[si], c->stream);
+            reduce<T>(c, 1, kOpStore, S, nullptr, false);
+            const Scalars<T> h = read_scalars<T>(c, S[0]);
+            if (sigma) *sigma = static_cast<double>(h.val[0]);
+        });
+    });
+}
+
+acg_status acg_interleaved_prec_kernel(const acg_context* c, acg_field* r, acg_field* z,
+                                       const acg_field* q, double alpha, double* r_norm,
+                                       double* kappa) {
+    return guarded([&] {
+        check_ctx(c);
+        for (const acg_field* f :
+             {static_cast<const acg_field*>(r), static_cast<const acg_field*>(z), q})
+            check_field(c, f, "interleaved_prec_kernel");
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, {
+            reset_tmp<T>(c, static_cast<T>(alpha));
+            auto S = tmp_scalars<T>(c);
+            for (size_t si = 0; si < c->slabs.size(); ++si) {
+                const Slab& s = c->slabs[si];
+                launch_fused_prec<T>(view<T>(c, si), c->fast(), static_cast<T*>(r->data(si)),
+                                     static_cast<T*>(z->data(si)), static_cast<const T*>(q->data(si)),
+                                     static_cast<T*>(s.part[0]), static_cast<T*>(s.part[1]), S[si],
+                                     static_cast<T*>(s.phi), c->stream);
+            }
+            for (Scalars<T>* s : S)
+                if (read_scalars<T>(c, s).pivot)
+                    fail(ACG_ERR_BREAKDOWN,
+                         "interleaved_prec_kernel: zero pivot in tridiagonal elimination");
+            reduce<T>(c, 2, kOpStore, S, nullptr, false);
+            const Scalars<T> h = read_scalars<T>(c, S[0]);
+            if (r_norm) *r_norm = static_cast<double>(std::sqrt(h.val[0]));
+            if (kappa) *kappa = static_cast<double>(h.val[1]);
+        });
+    });
+}
+
+void acg_solver_config_default(acg_solver_config* cfg) {
+    if (!cfg) return;
+    cfg->epsilon = 1e-5;
+    cfg->tau = 1e-20;
+    cfg->maxiter = 500;
+    cfg->variant = ACG_VARIANT_STANDARD;  // SolverConfig default (solver.hpp:23)
+    cfg->backend = ACG_BACKEND_MATRIX_FREE;
+    cfg->workers = 1;
+    cfg->record_timings = 0;
+}
+
+}  // extern "C"
+
+// ==================================================================== solver
+namespace {
+
+enum Family { kSpmv = 0, kPrec, kBlas, kFusedSpmv, kFusedPrec, kFamilies };
+
+struct EventTimer {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<size_t, size_t>> marks[kFamilies];
+    size_t open_idx = 0;
+    cudaEvent_t next() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void begin(int) {
+        if (!on) return;
+        open_idx = used;
+        CK(cudaEventRecord(next(), st));
+    }
+    void end(int fam) {
+        if (!on) return;
+        const size_t b = open_idx;
+        CK(cudaEventRecord(next(), st));
+        marks[fam].emplace_back(b, used - 1);
+    }
+    double seconds(int fam) {
+        double ms = 0;
+        for (auto& pr : marks[fam]) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, pool[pr.first], pool[pr.second]));
+            ms += t;
+        }
+        return ms * 1e-3;
+    }
+    int count(int fam) const { return static_cast<int>(marks[fam].size()); }
+    void reset() {
+        used = 0;
+        for (auto& m : marks) m.clear();
+    }
+    ~EventTimer() {
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+struct acg_solver {
+    const acg_context* ctx = nullptr;
+    acg_solver_config cfg{};
+    acg_field *u = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    const acg_field* f = nullptr;
+    std::vector<void*> S;     // Scalars<T>* per local slab
+    std::vector<double*> hist;  // 4 arrays per local slab
+    void* mirror = nullptr;   // pinned 2 x Scalars<T>
+    cudaEvent_t mev[2] = {nullptr, nullptr};
+    bool started = false;
+    long long launches0 = 0;
+    EventTimer timer;       // per-family timings (record_timings)
+    EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
+    std::chrono::steady_clock::time_point t0;
+    ~acg_solver() {
+        for (acg_field* fl : {u, r, z, p, q})
+            if (fl) free_field(fl);
+        for (void* s : S) cudaFree(s);
+        for (double* h : hist) cudaFree(h);
+        if (mirror) cudaFreeHost(mirror);
+        for (cudaEvent_t e : mev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+void validate(const acg_solver_config* cfg) {
+    if (!cfg) fail(ACG_ERR_INVALID_ARGUMENT, "null config");
+    // SolverConfig::validate, solver.hpp:27-35
+    if (!(cfg->epsilon > 0.0)) fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: epsilon must be > 0");
+    if (!(cfg->tau > 0.0)) fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: tau must be > 0");
+    if (cfg->maxiter < 1) fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: maxiter must be >= 1");
+    if (cfg->workers < 1) fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: workers must be >= 1");
+    if (cfg->variant == ACG_VARIANT_INTERLEAVED && cfg->backend == ACG_BACKEND_CSR)
+        fail(ACG_ERR_INVALID_ARGUMENT,
+             "SolverConfig: the interleaved variant exists for the matrix-free backend only");
+    if (cfg->backend == ACG_BACKEND_CSR)
+        fail(ACG_ERR_INVALID_ARGUMENT,
+             "SolverConfig: the CSR backend is not part of the B200 build (matrix-free only)");
+    if (cfg->variant != ACG_VARIANT_STANDARD && cfg->variant != ACG_VARIANT_INTERLEAVED)
+        fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: unknown variant");
+}
+
+template <typename T>
+std::vector<Scalars<T>*> sv(acg_solver* s) {
+    std::vector<Scalars<T>*> v;
+    for (void* p : s->S) v.push_back(static_cast<Scalars<T>*>(p));
+    return v;
+}
+
+template <typename T>
+void solver_alloc(acg_solver* s) {
+    const acg_context* c = s->ctx;
+    const int cap = s->cfg.maxiter + 2;
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, sizeof(Scalars<T>)));
+        s->S.push_back(p);
+        for (int a = 0; a < 4; ++a) {
+            double* h = nullptr;
+            CK(cudaMalloc(&h, cap * sizeof(double)));
+            s->hist.push_back(h);
+        }
+    }
+    CK(cudaHostAlloc(&s->mirror, 2 * sizeof(Scalars<T>), cudaHostAllocPortable));
+    for (auto& e : s->mev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->u = new_field(c);
+    s->r = new_field(c);
+    s->z = new_field(c);
+    s->p = new_field(c);
+    s->q = new_field(c);
+}
+
+template <typename T>
+void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
+    const acg_context* c = s->ctx;
+    s->t0 = std::chrono::steady_clock::now();
+    s->launches0 = g_launches;
+    s->f = f;
+    s->timer.st = c->stream;
+    s->ktimer.st = c->stream;
+    s->timer.on = s->cfg.record_timings != 0;
+    s->timer.reset();
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        Scalars<T> h{};
+        h.eps = s->cfg.epsilon;
+        h.tau = s->cfg.tau;
+        h.maxiter = s->cfg.maxiter;
+        h.it = 1;
+        h.h_res = s->hist[si * 4 + 0];
+        h.h_kap = s->hist[si * 4 + 1];
+        h.h_alp = s->hist[si * 4 + 2];
+        h.h_bet = s->hist[si * 4 + 3];
+        CK(cudaMemcpyAsync(s->S[si], &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    }
+    auto S = sv<T>(s);
+    // u = u0, r = f (solver.hpp:288-290)
+    if (u0)
+        op_copy<T>(c, u0, s->u, nullptr);
+    else
+        for (size_t si = 0; si < c->slabs.size(); ++si)
+            launch_fill<T>(c->slabs[si].n_loc, T(0), static_cast<T*>(s->u->data(si)), c->stream);
+    op_copy<T>(c, f, s->r, nullptr);
+    // q = A u; r = r - q; ||r0||  (:295-305)
+    s->timer.begin(kSpmv);
+    op_apply<T>(c, s->u, s->q, S[0]);
+    s->timer.end(kSpmv);
+    s->timer.begin(kBlas);
+    op_axpy<T>(c, T(-1), nullptr, -1, false, s->q, s->r, false);
+    op_dot<T>(c, s->r, s->r, kOpR0, S, true);
+    s->timer.end(kBlas);
+    // z = M^-1 r; kappa_old = <r,z>  (:313-323)
+    s->timer.begin(kPrec);
+    op_precondition<T>(c, s->r, s->z, S, S[0]);
+    s->timer.end(kPrec);
+    s->timer.begin(kBlas);
+    op_dot<T>(c, s->r, s->z, kOpKappa0, S, true);
+    s->timer.end(kBlas);
+    // p = z
+    op_copy<T>(c, s->z, s->p, &S);
+    if (s->cfg.variant == ACG_VARIANT_INTERLEAVED) {
+        // q = A p; sigma = <p,q>; alpha  (:325-336)
+        s->timer.begin(kSpmv);
+        op_apply<T>(c, s->p, s->q, S[0]);
+        s->timer.end(kSpmv);
+        s->timer.begin(kBlas);
+        op_dot<T>(c, s->p, s->q, kOpSigma0, S, true);
+        s->timer.end(kBlas);
+    }
+    CK(cudaPeekAtLastError());
+    s->started = true;
+}
+
+// One iteration of the interleaved loop (solver.hpp:338-365): two sweeps,
+// two reductions, all gated on the device-side `done` flag.
+template <typename T>
+void iterate_interleaved(acg_solver* s) {
+    const acg_context* c = s->ctx;
+    auto S = sv<T>(s);
+    s->timer.begin(kFusedPrec);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& sl = c->slabs[si];
+        s->ktimer.begin(kFusedPrec);
+        launch_fused_prec<T>(view<T>(c, si), c->fast(), static_cast<T*>(s->r->data(si)),
+                             static_cast<T*>(s->z->data(si)), static_cast<const T*>(s->q->data(si)),
+                             static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), S[si],
+                             static_cast<T*>(sl.phi), c->stream);
+        s->ktimer.end(kFusedPrec);
+    }
+    reduce<T>(c, 2, kOpIlPrec, S, nullptr, true);
+    s->timer.end(kFusedPrec);
+    s->timer.begin(kFusedSpmv);
+    halo(c, s->z);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        s->ktimer.begin(kFusedSpmv);
+        launch_fused_spmv<T>(view<T>(c, si), c->fast(), static_cast<T*>(s->u->data(si)),
+                             static_cast<T*>(s->p->data(si)), static_cast<T*>(s->q->data(si)),
+                             static_cast<const T*>(s->z->data(si)),
+                             static_cast<T*>(c->slabs[si].part[0]), S[si], c->stream);
+        s->ktimer.end(kFusedSpmv);
+    }
+    reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true);
+    s->timer.end(kFusedSpmv);
+}
+
+// One iteration of the standard loop (solver.hpp:217-262): 9 sweeps.
+template <typename T>
+void iterate_standard(acg_solver* s) {
+    const acg_context* c = s->ctx;
+    auto S = sv<T>(s);
+    s->timer.begin(kSpmv);
+    op_apply<T>(c, s->p, s->q, S[0]);
+    s->timer.end(kSpmv);
+    s->timer.begin(kBlas);
+    op_dot<T>(c, s->p, s->q, kOpStdSigma, S, true);
+    op_axpy<T>(c, T(0), &S, 0, false, s->p, s->u, true);  // u = alpha p + u
+    op_axpy<T>(c, T(0), &S, 0, true, s->q, s->r, true);   // r = (-alpha) q + r
+    op_dot<T>(c, s->r, s->r, kOpStdRnorm, S, true);
+    s->timer.end(kBlas);
+    s->timer.begin(kPrec);
+    op_precondition<T>(c, s->r, s->z, S, S[0]);
+    s->timer.end(kPrec);
+    s->timer.begin(kBlas);
+    op_dot<T>(c, s->r, s->z, kOpStdKappa, S, true);
+    for (size_t si = 0; si < c->slabs.size(); ++si)  // p = beta p
+        launch_scal<T>(c->slabs[si].n_loc, T(0), &S[si]->beta, static_cast<T*>(s->p->data(si)),
+                       S[si], c->stream);
+    op_axpy<T>(c, T(1), &S, -1, false, s->z, s->p, true);  // p = 1 z + p
+    s->timer.end(kBlas);
+}
+
+template <typename T>
+void solver_iterate(acg_solver* s, int n) {
+    for (int it = 0; it < n; ++it) {
+        if (s->cfg.variant == ACG_VARIANT_INTERLEAVED)
+            iterate_interleaved<T>(s);
+        else
+            iterate_standard<T>(s);
+    }
+    CK(cudaPeekAtLastError());
+}
+
+double bytes_per_iteration(const acg_context* c) {
+    const double n = static_cast<double>(c->m) * c->m * c->n_z;
+    return static_cast<double>(c->s) * (11.0 * n) / c->nslabs_total;
+}
+
+// Enqueue iterations in batches; poll the done flag of the batch before the
+// current one (pipelined, so the GPU never idles on the host).
+template <typename T>
+void solver_run(acg_solver* s) {
+    const acg_context* c = s->ctx;
+    const double est_us = std::max(2.0, bytes_per_iteration(c) / 4.0e3);
+    int batch = static_cast<int>(std::ceil(1500.0 / est_us));
+    batch = std::max(1, std::min(batch, 64));
+    Scalars<T>* mir = static_cast<Scalars<T>*>(s->mirror);
+    int enq = 0, b = 0;
+    // state after init
+    CK(cudaMemcpyAsync(&mir[1], s->S[0], sizeof(Scalars<T>), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(s->mev[1], c->stream));
+    CK(cudaEventSynchronize(s->mev[1]));
+    if (mir[1].done) return;
+    while (enq < s->cfg.maxiter) {
+        const int n = std::min(batch, s->cfg.maxiter - enq);
+        solver_iterate<T>(s, n);
+        enq += n;
+        CK(cudaMemcpyAsync(&mir[b & 1], s->S[0], sizeof(Scalars<T>), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaEventRecord(s->mev[b & 1], c->stream));
+        if (b > 0) {
+            CK(cudaEventSynchronize(s->mev[(b - 1) & 1]));
+            if (mir[(b - 1) & 1].done) break;
+        }
+        ++b;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+template <typename T>
+void solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, double* hr, double* hk,
+                   double* ha, double* hb) {
+    const acg_context* c = s->ctx;
+    auto S = sv<T>(s);
+    CK(cudaStreamSynchronize(c->stream));
+    Scalars<T> h = read_scalars<T>(c, S[0]);
+    if (h.error) {
+        const char* var = s->cfg.variant == ACG_VARIANT_INTERLEAVED ? "pcg_interleaved"
+                                                                    : "pcg_standard";
+        switch (h.error) {
+            case kErrPivotFused:
+                fail(ACG_ERR_BREAKDOWN,
+                     "interleaved_prec_kernel: zero pivot in tridiagonal elimination");
+            case kErrPivotPrecond:
+                fail(ACG_ERR_BREAKDOWN, "precondition: zero pivot in tridiagonal elimination");
+            case kErrKappa:
+                fail(ACG_ERR_BREAKDOWN, "%s: <r,z> not positive (preconditioner not SPD?)", var);
+            default:
+                fail(ACG_ERR_BREAKDOWN, "%s: <p,Ap> not positive (operator not SPD?)", var);
+        }
+    }
+    // lagged catch-up u += alpha p when the interleaved loop converged (solver.hpp:345-351)
+    if (s->cfg.variant == ACG_VARIANT_INTERLEAVED && h.converged && h.iterations >= 1) {
+        s->timer.begin(kBlas);
+        op_axpy<T>(c, T(0), &S, 0, false, s->p, s->u, false);
+        s->timer.end(kBlas);
+    }
+    const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - s->t0).count();
+    T tr = op_true_residual<T>(c, s->u, s->f);
+    if (u_out) op_copy<T>(c, s->u, u_out, nullptr);
+    if (res) {
+        std::memset(res, 0, sizeof(*res));
+        res->iterations = h.iterations;
+        res->converged = h.converged;
+        res->true_residual = static_cast<double>(tr);
+        res->n_residual = h.n_res;
+        res->n_kappa = h.n_kap;
+        res->n_alpha = h.n_alp;
+        res->n_beta = h.n_bet;
+        res->timings.total = total;
+        if (s->timer.on) {
+            CK(cudaStreamSynchronize(c->stream));
+            res->timings.spmv = s->timer.seconds(kSpmv);
+            res->timings.prec = s->timer.seconds(kPrec);
+            res->timings.blas = s->timer.seconds(kBlas);
+            res->timings.fused_spmv = s->timer.seconds(kFusedSpmv);
+            res->timings.fused_prec = s->timer.seconds(kFusedPrec);
+        }
+        res->kernel_launches = g_launches - s->launches0;
+    }
+    double* outs[4] = {hr, hk, ha, hb};
+    const int counts[4] = {h.n_res, h.n_kap, h.n_alp, h.n_bet};
+    for (int a = 0; a < 4; ++a)
+        if (outs[a] && counts[a] > 0)
+            CK(cudaMemcpyAsync(outs[a], s->hist[a], counts[a] * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+acg_status acg_solver_create(acg_solver** out, const acg_context* c, const acg_solver_config* cfg) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
+        validate(cfg);
+        DeviceGuard g(c->device);
+        auto s = std::make_unique<acg_solver>();
+        s->ctx = c;
+        s->cfg = *cfg;
+        ACG_TDISPATCH(c, solver_alloc<T>(s.get()));
+        *out = s.release();
+    });
+}
+
+acg_status acg_solver_destroy(acg_solver* s) {
+    return guarded([&] {
+        if (!s) return;
+        DeviceGuard g(s->ctx->device);
+        cudaStreamSynchronize(s->ctx->stream);
+        delete s;
+    });
+}
+
+acg_status acg_solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
+    return guarded([&] {
+        if (!s) fail(ACG_ERR_INVALID_ARGUMENT, "null solver");
+        const acg_context* c = s->ctx;
+        check_field(c, f, "solve");
+        if (u0) check_field(c, u0, "solve");
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, solver_start<T>(s, f, u0));
+    });
+}
+
+acg_status acg_solver_iterate(acg_solver* s, int n) {
+    return guarded([&] {
+        if (!s || !s->started) fail(ACG_ERR_INVALID_ARGUMENT, "solver not started");
+        DeviceGuard g(s->ctx->device);
+        ACG_TDISPATCH(s->ctx, solver_iterate<T>(s, n));
+    });
+}
+
+acg_status acg_solver_time_kernels(acg_solver* s, int enable) {
+    return guarded([&] {
+        if (!s) fail(ACG_ERR_INVALID_ARGUMENT, "null solver");
+        s->ktimer.on = enable != 0;
+        s->ktimer.reset();
+    });
+}
+
+acg_status acg_solver_kernel_times(acg_solver* s, int* n_prec, double* ms_prec, int* n_spmv,
+                                   double* ms_spmv) {
+    return guarded([&] {
+        if (!s) fail(ACG_ERR_INVALID_ARGUMENT, "null solver");
+        DeviceGuard g(s->ctx->device);
+        CK(cudaStreamSynchronize(s->ctx->stream));
+        if (n_prec) *n_prec = s->ktimer.count(kFusedPrec);
+        if (ms_prec) *ms_prec = s->ktimer.seconds(kFusedPrec) * 1e3;
+        if (n_spmv) *n_spmv = s->ktimer.count(kFusedSpmv);
+        if (ms_spmv) *ms_spmv = s->ktimer.seconds(kFusedSpmv) * 1e3;
+        s->ktimer.reset();
+    });
+}
+
+acg_status acg_solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, double* hr,
+                             double* hk, double* ha, double* hb) {
+    return guarded([&] {
+        if (!s || !s->started) fail(ACG_ERR_INVALID_ARGUMENT, "solver not started");
+        if (u_out) check_field(s->ctx, u_out, "solve");
+        DeviceGuard g(s->ctx->device);
+        ACG_TDISPATCH(s->ctx, solver_finish<T>(s, u_out, res, hr, hk, ha, hb));
+    });
+}
+
+acg_status acg_solve(const acg_context* c, const acg_field* f, const acg_field* u0,
+                     const acg_solver_config* cfg, acg_field* u_out, acg_solve_result* res,
+                     double* hr, double* hk, double* ha, double* hb) {
+    return guarded([&] {
+        check_ctx(c);
+        check_field(c, f, "solve");
+        if (u0) check_field(c, u0, "solve");
+        if (u_out) check_field(c, u_out, "solve");
+        validate(cfg);
+        DeviceGuard g(c->device);
+        acg_solver s;
+        s.ctx = c;
+        s.cfg = *cfg;
+        ACG_TDISPATCH(c, {
+            solver_alloc<T>(&s);
+            solver_start<T>(&s, f, u0);
+            solver_run<T>(&s);
+            solver_finish<T>(&s, u_out, res, hr, hk, ha, hb);
+        });
+    });
+}
+
+// ------------------------------------------------------- host entry points
+acg_status acg_apply_host(const acg_context* c, acg_layout layout, const void* x, void* y) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!x || !y) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
+        if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "apply: x and y must not alias");
+        DeviceGuard g(c->device);
+        PoolField fx(c), fy(c);
+        ACG_TDISPATCH(c, {
+            upload_t<T>(fx.f, x, layout, ACG_HOST_FULL);
+            op_apply<T>(c, fx.f, fy.f, nullptr);
+            download_t<T>(fy.f, y, layout, ACG_HOST_FULL);
+        });
+    });
+}
+
+acg_status acg_precondition_host(const acg_context* c, acg_layout layout, const void* y, void* x) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!x || !y) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
+        if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "precondition: y and x must not alias");
+        DeviceGuard g(c->device);
+        PoolField fy(c), fx(c);
+        ACG_TDISPATCH(c, {
+            upload_t<T>(fy.f, y, layout, ACG_HOST_FULL);
+            reset_tmp<T>(c);
+            auto S = tmp_scalars<T>(c);
+            op_precondition<T>(c, fy.f, fx.f, S, nullptr);
+            CK(cudaPeekAtLastError());
+            for (Scalars<T>* sp : S)
+                if (read_scalars<T>(c, sp).pivot)
+                    fail(ACG_ERR_BREAKDOWN, "precondition: zero pivot in tridiagonal elimination");
+            download_t<T>(fx.f, x, layout, ACG_HOST_FULL);
+        });
+    });
+}
+
+acg_status acg_true_residual_host(const acg_context* c, acg_layout layout, const void* u,
+                                  const void* f, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!u || !f || !out) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
+        DeviceGuard g(c->device);
+        PoolField fu(c), ff(c);
+        ACG_TDISPATCH(c, {
+            upload_t<T>(fu.f, u, layout, ACG_HOST_FULL);
+            upload_t<T>(ff.f, f, layout, ACG_HOST_FULL);
+            *out = static_cast<double>(op_true_residual<T>(c, fu.f, ff.f));
+        });
+    });
+}
+
+acg_status acg_solve_host(const acg_context* c, acg_layout layout, const void* f, const void* u0,
+                          const acg_solver_config* cfg, void* u_out, acg_solve_result* res,
+                          double* hr, double* hk, double* ha, double* hb) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!f || !u_out) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
+        validate(cfg);
+        DeviceGuard g(c->device);
+        PoolField ff(c), fu0(c), fu(c);
+        acg_solver s;
+        s.ctx = c;
+        s.cfg = *cfg;
+        ACG_TDISPATCH(c, {
+            upload_t<T>(ff.f, f, layout, ACG_HOST_FULL);
+            if (u0) upload_t<T>(fu0.f, u0, layout, ACG_HOST_FULL);
+            solver_alloc<T>(&s);
+            solver_start<T>(&s, ff.f, u0 ? fu0.f : nullptr);
+            solver_run<T>(&s);
+            solver_finish<T>(&s, fu.f, res, hr, hk, ha, hb);
+            download_t<T>(fu.f, u_out, layout, ACG_HOST_FULL);
+        });
+    });
+}
+
+}  // extern "C"
