@@ -300,13 +300,21 @@ def run_gpu(args, cfg):
         hu = capi.HostBuffer((ml, m, n_z), npdt)
         f.download(out=hf.array, scope=capi.HOST_LOCAL)
         f2, u2 = ctx.field(), ctx.field()
+        # one untimed warm-up call (allocates the context's cached solver state)
+        f2.upload(hf.array, scope=capi.HOST_LOCAL)
+        capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps)
+        u2.download(out=hu.array, scope=capi.HOST_LOCAL)
         barrier()
         t0 = time.perf_counter()
         f2.upload(hf.array, scope=capi.HOST_LOCAL)
+        ctx.sync()
+        t1 = time.perf_counter()
         r2 = capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps)
+        t2 = time.perf_counter()
         u2.download(out=hu.array, scope=capi.HOST_LOCAL)
         barrier()
         wall = time.perf_counter() - t0
+        split = {"upload_s": t1 - t0, "solve_s": t2 - t1, "download_s": time.perf_counter() - t2}
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([wall], device="cuda", dtype=torch.float64)
@@ -317,7 +325,7 @@ def run_gpu(args, cfg):
                "h2d_bytes_per_step": nbytes * world / args.steps,
                "d2h_bytes_per_step": nbytes * world / args.steps + 8 * (args.steps + 1),
                "call": "acg_field_upload + acg_solve + acg_field_download (pinned host)",
-               "solve_wall_s": wall, "iterations": r2["iterations"]}
+               "solve_wall_s": wall, "iterations": r2["iterations"], "split": split}
         f2.close()
         u2.close()
         hf.close()

@@ -112,6 +112,12 @@ typedef struct {
 
 acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_operator_desc* desc,
                               const acg_placement* placement);
+
+/* The i-slab decomposition a context with p slabs uses (host only, no GPU):
+ * slab s owns i-planes [i_begin[s], i_begin[s+1]); *exact_tree = 1 when the slabs
+ * are nodes of the reference's pairwise reduction tree (parallel.hpp:11-20), so
+ * the multi-slab reductions are bit-identical to the single-device ones. */
+acg_status acg_partition_plan(int m, int p, int* i_begin /* p+1 */, int* exact_tree);
 acg_status acg_context_destroy(acg_context* ctx);
 
 typedef struct {

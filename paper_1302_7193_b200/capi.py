@@ -13,7 +13,7 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libacg_cuda.so")
+LIB_PATH = os.environ.get("ACG_LIB_OVERRIDE") or os.path.join(_HERE, "libacg_cuda.so")
 
 F64, F32 = 0, 1
 VERTICAL, HORIZONTAL = 0, 1
@@ -90,6 +90,7 @@ def lib():
         "acg_comm_destroy": (ip, [vp]),
         "acg_context_create": (ip, [pp, ip, C.POINTER(OperatorDesc), C.POINTER(Placement)]),
         "acg_context_destroy": (ip, [vp]),
+        "acg_partition_plan": (ip, [ip, ip, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "acg_context_info_get": (ip, [vp, C.POINTER(ContextInfo)]),
         "acg_context_stream": (vp, [vp]),
         "acg_synchronize": (ip, [vp]),
@@ -137,6 +138,14 @@ def exported_symbols():
     """Names of the C-ABI functions this wrapper binds (all declared in acg.h)."""
     lib()
     return [n for n in dir(_lib) if n.startswith("acg_")]
+
+
+def partition_plan(m, p):
+    """(i_begin[0..p], exact_tree) of the p-slab decomposition (acg_partition_plan)."""
+    ib = (C.c_int * (p + 1))()
+    ex = C.c_int()
+    check(lib().acg_partition_plan(m, p, ib, C.byref(ex)))
+    return list(ib), bool(ex.value)
 
 
 def check(status):

@@ -699,14 +699,23 @@ void ensure_smem(KernelT kernel, size_t bytes) {
 // Thomas launch configuration (warps per block, phi checkpoint stride, cp.async
 // depth), chosen per precision; ACG_THOMAS_OCC pads shared memory to cap the
 // resident blocks per SM (L2-footprint experiments).
-using ThomasF64 = ThomasCfg<2, 2, 12>;
-using ThomasF32 = ThomasCfg<2, 1, 12>;
+using ThomasF64 = ThomasCfg<4, 4, 7>;
+using ThomasF32 = ThomasCfg<4, 2, 7>;
 template <typename T>
 struct ThomasOf;
 template <>
 struct ThomasOf<double> { using type = ThomasF64; };
 template <>
 struct ThomasOf<float> { using type = ThomasF32; };
+
+// ACG_L2_HINTS=0 disables the L2 eviction-priority hints (A/B experiments).
+inline int l2_hints() {
+    static int h = [] {
+        const char* e = std::getenv("ACG_L2_HINTS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return h;
+}
 
 inline size_t thomas_pad(size_t bytes) {
     static int occ = [] {
@@ -726,8 +735,15 @@ void launch_thomas_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T
     const dim3 block(32, C::W);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + C::W - 1) / C::W);
     const size_t smem = thomas_pad(thomas_smem_bytes<T, C>(v.n_z, phi_scratch != nullptr));
-    ensure_smem(k_thomas<T, Fast, Fused, C>, smem);
-    k_thomas<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch);
+    if (phi_scratch) {
+        ensure_smem(k_thomas<T, Fast, Fused, C, true>, smem);
+        k_thomas<T, Fast, Fused, C, true>
+            <<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch, l2_hints());
+    } else {
+        ensure_smem(k_thomas<T, Fast, Fused, C, false>, smem);
+        k_thomas<T, Fast, Fused, C, false>
+            <<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch, l2_hints());
+    }
 }
 
 // ACG_THOMAS="W,CP,D" selects one of the compiled configurations (tuning sweeps).
@@ -736,8 +752,8 @@ inline int thomas_choice() {
         const char* e = std::getenv("ACG_THOMAS");
         if (!e) return 0;
         const std::string s(e);
-        const char* names[] = {"", "2,2,12", "2,4,12", "2,4,8", "4,4,8", "2,8,8", "2,1,12", "4,2,8"};
-        for (int a = 1; a < 8; ++a)
+        const char* names[] = {"", "2,4,7", "4,4,7", "2,8,7", "4,8,7", "2,2,7", "4,4,5", "8,4,7", "4,2,7", "8,2,7"};
+        for (int a = 1; a < 10; ++a)
             if (s == names[a]) return a;
         return 0;
     }();
@@ -749,13 +765,15 @@ void launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk
                    const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
 #define ACG_TH(...) launch_thomas_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, phi_scratch, st)
     switch (thomas_choice()) {
-        case 1: ACG_TH(ThomasCfg<2, 2, 12>); break;
-        case 2: ACG_TH(ThomasCfg<2, 4, 12>); break;
-        case 3: ACG_TH(ThomasCfg<2, 4, 8>); break;
-        case 4: ACG_TH(ThomasCfg<4, 4, 8>); break;
-        case 5: ACG_TH(ThomasCfg<2, 8, 8>); break;
-        case 6: ACG_TH(ThomasCfg<2, 1, 12>); break;
-        case 7: ACG_TH(ThomasCfg<4, 2, 8>); break;
+        case 1: ACG_TH(ThomasCfg<2, 4, 7>); break;
+        case 2: ACG_TH(ThomasCfg<4, 4, 7>); break;
+        case 3: ACG_TH(ThomasCfg<2, 8, 7>); break;
+        case 4: ACG_TH(ThomasCfg<4, 8, 7>); break;
+        case 5: ACG_TH(ThomasCfg<2, 2, 7>); break;
+        case 6: ACG_TH(ThomasCfg<4, 4, 5>); break;
+        case 7: ACG_TH(ThomasCfg<8, 4, 7>); break;
+        case 8: ACG_TH(ThomasCfg<4, 2, 7>); break;
+        case 9: ACG_TH(ThomasCfg<8, 2, 7>); break;
         default: ACG_TH(typename ThomasOf<T>::type); break;
     }
 #undef ACG_TH

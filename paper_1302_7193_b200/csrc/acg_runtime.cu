@@ -168,6 +168,7 @@ struct acg_context {
     void* gather = nullptr;       // nslabs_total * 4 T
     void* gather_send = nullptr;  // 4 T (NCCL)
     std::vector<acg_field*> pool; // reusable scratch fields (host entry points)
+    acg_solver* cached = nullptr; // solver state reused by acg_solve / acg_solve_host
     size_t s = 8;
     bool fast() const { return math == ACG_MATH_FAST; }
 };
@@ -315,6 +316,8 @@ void* alloc_tmp_scalars() {
 
 }  // namespace
 
+void destroy_cached_solver(acg_context* c);  // defined after acg_solver
+
 // =================================================================== basics
 extern "C" {
 
@@ -452,11 +455,25 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
     });
 }
 
+acg_status acg_partition_plan(int m, int p, int* i_begin, int* exact_tree) {
+    return guarded([&] {
+        if (m < 1 || p < 1 || p > m || !i_begin || !exact_tree)
+            fail(ACG_ERR_INVALID_ARGUMENT, "partition_plan: bad arguments");
+        std::vector<std::pair<int, int>> parts;
+        bool exact = false;
+        partition(m, p, parts, exact);
+        for (int s = 0; s < p; ++s) i_begin[s] = parts[s].first;
+        i_begin[p] = parts[p - 1].second;
+        *exact_tree = exact ? 1 : 0;
+    });
+}
+
 acg_status acg_context_destroy(acg_context* c) {
     return guarded([&] {
         if (!c) return;
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
+        destroy_cached_solver(c);
         for (acg_field* f : c->pool) {
             for (void* b : f->base) cudaFree(b);
             delete f;
@@ -504,15 +521,23 @@ void* acg_context_stream(const acg_context* c) { return c ? c->stream : nullptr;
 // ==================================================================== fields
 namespace {
 
-acg_field* new_field(const acg_context* c) {
+// zero_all: the public Field3D contract (zero-filled); internal work fields only
+// need their two ghost planes cleared (the owned planes are always written first).
+acg_field* new_field(const acg_context* c, bool zero_all = true) {
     auto f = std::make_unique<acg_field>();
     f->ctx = c;
     for (const Slab& s : c->slabs) {
         void* p = nullptr;
         const size_t bytes = static_cast<size_t>(s.n_loc + 2 * s.plane) * c->s;
+        const size_t pb = static_cast<size_t>(s.plane) * c->s;
         CK(cudaMalloc(&p, bytes));
         f->base.push_back(p);
-        CK(cudaMemsetAsync(p, 0, bytes, c->stream));
+        if (zero_all) {
+            CK(cudaMemsetAsync(p, 0, bytes, c->stream));
+        } else {
+            CK(cudaMemsetAsync(p, 0, pb, c->stream));
+            CK(cudaMemsetAsync(static_cast<char*>(p) + bytes - pb, 0, pb, c->stream));
+        }
     }
     return f.release();
 }
@@ -1095,6 +1120,7 @@ struct acg_solver {
     void* mirror = nullptr;   // pinned 2 x Scalars<T>
     cudaEvent_t mev[2] = {nullptr, nullptr};
     bool started = false;
+    int cap = 0;              // history capacity (entries)
     long long launches0 = 0;
     EventTimer timer;       // per-family timings (record_timings)
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
@@ -1109,6 +1135,11 @@ struct acg_solver {
             if (e) cudaEventDestroy(e);
     }
 };
+
+void destroy_cached_solver(acg_context* c) {
+    delete c->cached;
+    c->cached = nullptr;
+}
 
 namespace {
 
@@ -1139,7 +1170,8 @@ std::vector<Scalars<T>*> sv(acg_solver* s) {
 template <typename T>
 void solver_alloc(acg_solver* s) {
     const acg_context* c = s->ctx;
-    const int cap = s->cfg.maxiter + 2;
+    const int cap = std::max(s->cfg.maxiter + 2, 4096);
+    s->cap = cap;
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         void* p = nullptr;
         CK(cudaMalloc(&p, sizeof(Scalars<T>)));
@@ -1152,11 +1184,33 @@ void solver_alloc(acg_solver* s) {
     }
     CK(cudaHostAlloc(&s->mirror, 2 * sizeof(Scalars<T>), cudaHostAllocPortable));
     for (auto& e : s->mev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    s->u = new_field(c);
-    s->r = new_field(c);
-    s->z = new_field(c);
-    s->p = new_field(c);
-    s->q = new_field(c);
+    s->u = new_field(c, false);
+    s->r = new_field(c, false);
+    s->z = new_field(c, false);
+    s->p = new_field(c, false);
+    s->q = new_field(c, false);
+}
+
+// Solver state cached in the context between solve calls (the five work
+// fields alone are 5 x N x s bytes; re-allocating them per call dominated the
+// end-to-end time of repeated solves).
+template <typename T>
+acg_solver* cached_solver(const acg_context* c, const acg_solver_config* cfg) {
+    acg_context* cc = const_cast<acg_context*>(c);
+    if (cc->cached && cc->cached->cap < cfg->maxiter + 2) {
+        delete cc->cached;
+        cc->cached = nullptr;
+    }
+    if (!cc->cached) {
+        auto s = std::make_unique<acg_solver>();
+        s->ctx = c;
+        s->cfg = *cfg;
+        solver_alloc<T>(s.get());
+        cc->cached = s.release();
+    }
+    cc->cached->cfg = *cfg;
+    cc->cached->started = false;
+    return cc->cached;
 }
 
 template <typename T>
@@ -1472,14 +1526,11 @@ acg_status acg_solve(const acg_context* c, const acg_field* f, const acg_field* 
         if (u_out) check_field(c, u_out, "solve");
         validate(cfg);
         DeviceGuard g(c->device);
-        acg_solver s;
-        s.ctx = c;
-        s.cfg = *cfg;
         ACG_TDISPATCH(c, {
-            solver_alloc<T>(&s);
-            solver_start<T>(&s, f, u0);
-            solver_run<T>(&s);
-            solver_finish<T>(&s, u_out, res, hr, hk, ha, hb);
+            acg_solver* s = cached_solver<T>(c, cfg);
+            solver_start<T>(s, f, u0);
+            solver_run<T>(s);
+            solver_finish<T>(s, u_out, res, hr, hk, ha, hb);
         });
     });
 }
@@ -1545,16 +1596,13 @@ acg_status acg_solve_host(const acg_context* c, acg_layout layout, const void* f
         validate(cfg);
         DeviceGuard g(c->device);
         PoolField ff(c), fu0(c), fu(c);
-        acg_solver s;
-        s.ctx = c;
-        s.cfg = *cfg;
         ACG_TDISPATCH(c, {
             upload_t<T>(ff.f, f, layout, ACG_HOST_FULL);
             if (u0) upload_t<T>(fu0.f, u0, layout, ACG_HOST_FULL);
-            solver_alloc<T>(&s);
-            solver_start<T>(&s, ff.f, u0 ? fu0.f : nullptr);
-            solver_run<T>(&s);
-            solver_finish<T>(&s, fu.f, res, hr, hk, ha, hb);
+            acg_solver* s = cached_solver<T>(c, cfg);
+            solver_start<T>(s, ff.f, u0 ? fu0.f : nullptr);
+            solver_run<T>(s);
+            solver_finish<T>(s, fu.f, res, hr, hk, ha, hb);
             download_t<T>(fu.f, u_out, layout, ACG_HOST_FULL);
         });
     });
