@@ -128,6 +128,8 @@ typedef struct {
     int i_begin, i_end; /* i-range owned by this process */
     int exact_tree;     /* 1 if reductions reproduce the reference tree bit-for-bit */
     size_t bytes_per_field_local;
+    int thomas_tmem;    /* 1 if the Thomas sweeps keep z' in TMEM with branch-free
+                           divisions (their operand ranges validated at creation) */
 } acg_context_info;
 acg_status acg_context_info_get(const acg_context* ctx, acg_context_info* out);
 acg_status acg_synchronize(const acg_context* ctx);

@@ -46,7 +46,7 @@ class ContextInfo(C.Structure):
     _fields_ = [("m", C.c_int), ("n_z", C.c_int), ("dtype", C.c_int), ("math", C.c_int),
                 ("nslabs_total", C.c_int), ("nslabs_local", C.c_int), ("rank", C.c_int),
                 ("i_begin", C.c_int), ("i_end", C.c_int), ("exact_tree", C.c_int),
-                ("bytes_per_field_local", C.c_size_t)]
+                ("bytes_per_field_local", C.c_size_t), ("thomas_tmem", C.c_int)]
 
 
 class SolverConfig(C.Structure):

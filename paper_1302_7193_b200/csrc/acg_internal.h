@@ -44,6 +44,7 @@ struct SlabView {
     long long plane;  // n_z * m
     const T* prof;    // kProfRows x n_z
     const T* col;     // kColRows x (m_loc * m)
+    int tm_ok;        // host side: the TMEM Thomas sweep's division ranges hold (k_validate_tm)
 };
 
 // Reasons a solve stops with NumericalBreakdown (operator.hpp:21-24,
@@ -106,6 +107,10 @@ extern long long g_launches;  // kernel launches issued (all entry points)
 template <typename T>
 void launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
                        T* part_k, Scalars<T>* S, T* phi_scratch, cudaStream_t st);
+// Once per slab: may the sweeps use the TMEM kernel with common-path
+// divisions (k_validate_tm)? Synchronous.
+template <typename T>
+bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st);
 template <typename T>
 void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scalars<T>* S,
                          const Scalars<T>* gate, T* phi_scratch, cudaStream_t st);

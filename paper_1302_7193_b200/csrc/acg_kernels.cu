@@ -118,6 +118,7 @@ __device__ __forceinline__ Col<T> load_col(const SlabView<T>& v, int il, int j) 
 
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
+#include "acg_thomas_tm.cuh"
 
 // ================================================================ K2 / K3 / K8
 constexpr int kStencilWarps = 8;
@@ -760,9 +761,55 @@ inline int thomas_choice() {
     return c;
 }
 
+// TMEM-resident sweep (k_thomas_tm). Shared memory is padded so that no more
+// CTAs become resident on an SM than its 512 TMEM columns can serve (a CTA
+// beyond that would only wait inside tcgen05.alloc).
+template <typename T, bool Fast, bool Fused, class C>
+void launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
+                          Scalars<T>* S, const Scalars<T>* gate, cudaStream_t st) {
+    const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
+    const dim3 block(32, C::W);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + C::W - 1) / C::W);
+    size_t smem = thomas_tm_smem_bytes<T, C>(v.n_z);
+    const size_t max_ctas = 512u / tcols;
+    const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
+    if (smem < floor_bytes) smem = floor_bytes;
+    ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
+    k_thomas_tm<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, tcols);
+}
+
+// ACG_THOMAS_TM="CP,D" selects a compiled TMEM configuration; "0" disables
+// the TMEM sweep (A/B experiments).
+inline int thomas_tm_choice() {
+    static int c = [] {
+        const char* e = std::getenv("ACG_THOMAS_TM");
+        if (!e) return 1;
+        const std::string s(e);
+        const char* names[] = {"0", "2,7", "4,7", "2,8", "4,8", "2,5", "4,5"};
+        for (int a = 0; a < 7; ++a)
+            if (s == names[a]) return a;
+        return 1;
+    }();
+    return c;
+}
+
 template <typename T, bool Fast, bool Fused>
 void launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
                    const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
+    const int tmc = thomas_tm_choice();
+    if (tmc != 0 && v.tm_ok && phi_scratch == nullptr && thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
+#define ACG_TM(...) launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, st)
+        switch (tmc) {
+            case 2: ACG_TM(ThomasTmCfg<4, 7>); break;
+            case 3: ACG_TM(ThomasTmCfg<2, 8>); break;
+            case 4: ACG_TM(ThomasTmCfg<4, 8>); break;
+            case 5: ACG_TM(ThomasTmCfg<2, 5>); break;
+            case 6: ACG_TM(ThomasTmCfg<4, 5>); break;
+            default: ACG_TM(ThomasTmCfg<2, 7>); break;
+        }
+#undef ACG_TM
+        return;
+    }
 #define ACG_TH(...) launch_thomas_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, phi_scratch, st)
     switch (thomas_choice()) {
         case 1: ACG_TH(ThomasCfg<2, 4, 7>); break;
@@ -796,6 +843,21 @@ TreePlan make_tree_plan(long long n) {
 size_t thomas_smem_per_block(int dsize, int n_z, bool global_phi) {
     return dsize == 4 ? thomas_smem_bytes<float, ThomasF32>(n_z, global_phi)
                       : thomas_smem_bytes<double, ThomasF64>(n_z, global_phi);
+}
+
+template <typename T>
+bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st) {
+    int* bad = nullptr;
+    if (cudaMalloc(&bad, sizeof(int)) != cudaSuccess) return false;
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    const long long ncol = static_cast<long long>(v.m_loc) * v.m;
+    k_validate_tm<T><<<grid_1d(ncol, 128), 128, 0, st>>>(v, bad);
+    post_launch("validate_tm");
+    int h = 1;
+    cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    const bool ok = cudaStreamSynchronize(st) == cudaSuccess && h == 0;
+    cudaFree(bad);
+    return ok;
 }
 
 template <typename T>
@@ -960,6 +1022,7 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
 }
 
 #define ACG_INSTANTIATE(T)                                                                      \
+    template bool validate_thomas_tm<T>(const SlabView<T>&, cudaStream_t);                      \
     template void launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,      \
                                        Scalars<T>*, T*, cudaStream_t);                          \
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \

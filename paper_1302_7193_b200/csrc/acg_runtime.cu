@@ -135,6 +135,7 @@ struct Slab {
     void* staging = nullptr;
     void* tmp = nullptr;  // Scalars<T> for API calls
     TreePlan plan{};
+    bool tm_ok = false;   // TMEM Thomas sweep usable (validate_thomas_tm)
 };
 
 size_t dsize(acg_dtype t) { return t == ACG_F32 ? sizeof(float) : sizeof(double); }
@@ -207,6 +208,7 @@ SlabView<T> view(const acg_context* c, size_t si) {
     v.plane = s.plane;
     v.prof = static_cast<const T*>(s.prof);
     v.col = static_cast<const T*>(s.col);
+    v.tm_ok = s.tm_ok ? 1 : 0;
     return v;
 }
 
@@ -434,9 +436,11 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
             if (dtype == ACG_F32) {
                 build_slab_tables<float>(c.get(), s, d);
                 s.tmp = alloc_tmp_scalars<float>();
+                s.tm_ok = validate_thomas_tm<float>(view<float>(c.get(), a), c->stream);
             } else {
                 build_slab_tables<double>(c.get(), s, d);
                 s.tmp = alloc_tmp_scalars<double>();
+                s.tm_ok = validate_thomas_tm<double>(view<double>(c.get(), a), c->stream);
             }
             const long long ncol = static_cast<long long>(s.m_loc) * d->m;
             for (int a2 = 0; a2 < 3; ++a2) CK(cudaMalloc(&s.part[a2], ncol * c->s));
@@ -503,6 +507,9 @@ acg_status acg_context_info_get(const acg_context* c, acg_context_info* o) {
         size_t b = 0;
         for (const Slab& s : c->slabs) b += static_cast<size_t>(s.n_loc) * c->s;
         o->bytes_per_field_local = b;
+        o->thomas_tmem = 1;
+        for (const Slab& s : c->slabs)
+            if (!s.tm_ok) o->thomas_tmem = 0;
     });
 }
 

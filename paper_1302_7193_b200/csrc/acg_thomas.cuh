@@ -355,3 +355,4 @@ __global__ void __launch_bounds__(C::NT)
         part_k[cidx] = kap;
     }
 }
+

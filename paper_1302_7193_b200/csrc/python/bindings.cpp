@@ -164,6 +164,7 @@ void bind_context(py::module_& mod, const char* name) {
             d["slabs"] = i.nslabs_total;
             d["exact_tree"] = static_cast<bool>(i.exact_tree);
             d["bytes_per_field"] = i.bytes_per_field_local;
+            d["thomas_tmem"] = static_cast<bool>(i.thomas_tmem);
             return d;
         });
     (void)sizeof(Cls);
