@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(32 * kStencilWarps)
 // neighbours are plain loads that hit L1/L2 (the rows belong to adjacent warps).
 constexpr int kSpmvD = 6;
 
-template <typename T, bool Fast>
+// X: warps of a CTA along j (X = 1: 8 i-planes x 32 j; X = 8: 1 plane x 256 j).
+template <typename T, bool Fast, int X = 1>
 __global__ void __launch_bounds__(32 * kStencilWarps)
     k_fused_spmv_ring(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
@@ -193,8 +194,8 @@ __global__ void __launch_bounds__(32 * kStencilWarps)
     const int tid = threadIdx.y * 32 + threadIdx.x;
     load_profile(prof, v.prof, 4 * n_z, tid, NT);
     __syncthreads();
-    const int j = blockIdx.x * 32 + threadIdx.x;
-    const int il = blockIdx.y * kStencilWarps + threadIdx.y;
+    const int j = (blockIdx.x * X + threadIdx.y % X) * 32 + threadIdx.x;
+    const int il = blockIdx.y * (kStencilWarps / X) + threadIdx.y / X;
     if (j >= m || il >= v.m_loc) return;
     T* ring = prof + 4 * n_z;
     const T* sP = prof + kProfS * n_z;
@@ -223,9 +224,19 @@ __global__ void __launch_bounds__(32 * kStencilWarps)
     }
     int cs = 0, ps_ = D;
     T z0 = zc[0], zd = z0, sig = T(0);
+    // horizontal neighbours are loaded one level ahead (their L1/L2 latency then
+    // overlaps a whole level of work instead of stalling it)
+    T ze = zc[c.oe], zw = zc[c.ow], zn = zc[c.on], zs = zc[c.os];
     for (int k = 0; k < n_z; ++k) {
         const long long l = static_cast<long long>(k) * m;
-        const T ze = zc[l + c.oe], zw = zc[l + c.ow], zn = zc[l + c.on], zs = zc[l + c.os];
+        const T ce = ze, cw = zw, cn = zn, cs_ = zs;
+        if (k + 1 < n_z) {
+            const long long l1 = l + m;
+            ze = zc[l1 + c.oe];
+            zw = zc[l1 + c.ow];
+            zn = zc[l1 + c.on];
+            zs = zc[l1 + c.os];
+        }
         cp_wait<D - 1>();
         T pv = *slot(cs, 0), qv = *slot(cs, 1);
         const T uv = *slot(cs, 2);
@@ -239,7 +250,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps)
         qv = A::mul(beta, qv);
         __stcs(pc + l, pv);
         const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an, c.as,
-                                      z0, zu, zd, ze, zw, zn, zs);
+                                      z0, zu, zd, ce, cw, cn, cs_);
         qv = A::add(qv, A::mul(dP[k], dq));
         sig = A::add(sig, A::mul(pv, qv));
         __stcs(qc + l, qv);
@@ -689,6 +700,8 @@ inline void post_launch(const char* what) {
     }
 }
 
+#include "acg_stencil_tile.cuh"
+
 template <typename KernelT>
 void ensure_smem(KernelT kernel, size_t bytes) {
     if (bytes > 48 * 1024)
@@ -769,7 +782,8 @@ void launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
                           Scalars<T>* S, const Scalars<T>* gate, cudaStream_t st) {
     const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
     const dim3 block(32, C::W);
-    const dim3 grid((v.m + 31) / 32, (v.m_loc + C::W - 1) / C::W);
+    constexpr int PW = C::W / C::X;  // i-planes per CTA
+    const dim3 grid((v.m + 32 * C::X - 1) / (32 * C::X), (v.m_loc + PW - 1) / PW);
     size_t smem = thomas_tm_smem_bytes<T, C>(v.n_z);
     const size_t max_ctas = 512u / tcols;
     const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
@@ -778,15 +792,15 @@ void launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
     k_thomas_tm<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, tcols);
 }
 
-// ACG_THOMAS_TM="CP,D" selects a compiled TMEM configuration; "0" disables
+// ACG_THOMAS_TM="CP,D,DB" selects a compiled TMEM configuration; "0" disables
 // the TMEM sweep (A/B experiments).
 inline int thomas_tm_choice() {
     static int c = [] {
         const char* e = std::getenv("ACG_THOMAS_TM");
         if (!e) return 1;
         const std::string s(e);
-        const char* names[] = {"0", "2,7", "4,7", "2,8", "4,8", "2,5", "4,5"};
-        for (int a = 0; a < 7; ++a)
+        const char* names[] = {"0", "4,15,15", "4,15,15,1", "4,15,15,2", "8,15,15", "4,12,12", "2,15,15", "4,15,8"};
+        for (int a = 0; a < 8; ++a)
             if (s == names[a]) return a;
         return 1;
     }();
@@ -800,12 +814,13 @@ void launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk
     if (tmc != 0 && v.tm_ok && phi_scratch == nullptr && thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
 #define ACG_TM(...) launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, st)
         switch (tmc) {
-            case 2: ACG_TM(ThomasTmCfg<4, 7>); break;
-            case 3: ACG_TM(ThomasTmCfg<2, 8>); break;
-            case 4: ACG_TM(ThomasTmCfg<4, 8>); break;
-            case 5: ACG_TM(ThomasTmCfg<2, 5>); break;
-            case 6: ACG_TM(ThomasTmCfg<4, 5>); break;
-            default: ACG_TM(ThomasTmCfg<2, 7>); break;
+            case 2: ACG_TM(ThomasTmCfg<4, 15, 15, 1>); break;
+            case 3: ACG_TM(ThomasTmCfg<4, 15, 15, 2>); break;
+            case 4: ACG_TM(ThomasTmCfg<8, 15, 15>); break;
+            case 5: ACG_TM(ThomasTmCfg<4, 12, 12>); break;
+            case 6: ACG_TM(ThomasTmCfg<2, 15, 15>); break;
+            case 7: ACG_TM(ThomasTmCfg<4, 15, 8>); break;
+            default: ACG_TM(ThomasTmCfg<4, 15, 15>); break;
         }
 #undef ACG_TM
         return;
@@ -885,11 +900,21 @@ void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const 
                        const Scalars<T>* S, cudaStream_t st) {
     const dim3 block(32, kStencilWarps);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
-    static const bool plain = [] {
+    // ACG_SPMV=plain|ring|tile overrides the variant; ACG_SPMV_D the tile prefetch depth,
+    // ACG_SPMV_X the ring kernel's warps along j.
+    // Default: the cp.async ring for fp64, shared z tiles for fp32 (measured, C3 / C4).
+    static const int mode = [] {
         const char* e = std::getenv("ACG_SPMV");
-        return e && std::string(e) == "plain";
+        if (e && std::string(e) == "plain") return 1;
+        if (e && std::string(e) == "ring") return 2;
+        if (e && std::string(e) == "tile") return 0;
+        return sizeof(T) == 4 ? 0 : 2;
     }();
-    if (plain) {
+    static const int tile_d = [] {
+        const char* e = std::getenv("ACG_SPMV_D");
+        return e ? std::atoi(e) : 5;
+    }();
+    if (mode == 1) {
         const size_t smem = sizeof(T) * 4 * static_cast<size_t>(v.n_z);
         if (fast) {
             ensure_smem(k_fused_spmv<T, true>, smem);
@@ -898,16 +923,39 @@ void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const 
             ensure_smem(k_fused_spmv<T, false>, smem);
             k_fused_spmv<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
         }
-    } else {
+    } else if (mode == 2) {
         const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                          static_cast<size_t>(kSpmvD + 1) * 4 * 32 * kStencilWarps);
+        static const int X = [] {
+            const char* e = std::getenv("ACG_SPMV_X");
+            return e ? std::atoi(e) : 8;
+        }();
+#define ACG_RX(F, XX)                                                                             \
+    do {                                                                                          \
+        const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
+                      (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
+        ensure_smem(k_fused_spmv_ring<T, F, XX>, smem);                                           \
+        k_fused_spmv_ring<T, F, XX><<<g2, block, smem, st>>>(v, u, p, q, z, part, S);             \
+    } while (0)
         if (fast) {
-            ensure_smem(k_fused_spmv_ring<T, true>, smem);
-            k_fused_spmv_ring<T, true><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+            if (X == 2) ACG_RX(true, 2); else if (X == 4) ACG_RX(true, 4); else if (X == 8) ACG_RX(true, 8); else ACG_RX(true, 1);
         } else {
-            ensure_smem(k_fused_spmv_ring<T, false>, smem);
-            k_fused_spmv_ring<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+            if (X == 2) ACG_RX(false, 2); else if (X == 4) ACG_RX(false, 4); else if (X == 8) ACG_RX(false, 8); else ACG_RX(false, 1);
         }
+#undef ACG_RX
+    } else {
+        const size_t smem = spmv_tile_smem_bytes<T, kStencilWarps>(v.n_z);
+#define ACG_SP(F, DD)                                                                   \
+    do {                                                                                \
+        ensure_smem(k_fused_spmv_tile<T, F, kStencilWarps, DD>, smem);                  \
+        k_fused_spmv_tile<T, F, kStencilWarps, DD><<<grid, block, smem, st>>>(v, u, p, q, z, part, S); \
+    } while (0)
+        if (fast) {
+            if (tile_d == 4) ACG_SP(true, 4); else if (tile_d == 6) ACG_SP(true, 6); else ACG_SP(true, 5);
+        } else {
+            if (tile_d == 4) ACG_SP(false, 4); else if (tile_d == 6) ACG_SP(false, 6); else ACG_SP(false, 5);
+        }
+#undef ACG_SP
     }
     post_launch("fused_spmv");
 }

@@ -1,0 +1,151 @@
+// K2 with the stencil input staged as shared-memory tiles (included by
+// acg_kernels.cu after the K2/K3 definitions).
+//
+//   k_fused_spmv_tile   interleaved_spmv_kernel   operator.hpp:214-266 (Alg. 2)
+//
+// k_fused_spmv_ring streams p, q, u and z(k+1) through a per-thread cp.async
+// ring but reads the four horizontal z neighbours with plain loads; those L1/L2
+// round trips sit on every level's critical path and were the dominant stall
+// (ncu: one DMUL waiting on them held half the warp samples). Here a CTA of
+// W warps (W i-planes x 32 j) copies, for every level, the z tile it needs
+// including a one-cell halo, (W+2) x 34 values, into a shared ring D levels
+// ahead; every neighbour is then a shared-memory load. A CTA barrier per level
+// publishes the tile (each value is copied by one thread and read by up to
+// five). DRAM traffic is unchanged (halo rows come from L2): u, p, q R+W, z R.
+// Arithmetic and association are those of k_fused_spmv (bit-identical).
+template <int W>
+struct SpmvTile {
+    static constexpr int R = W + 2, CW = 34, N = R * CW, NT = 32 * W, NS = 8;
+};
+
+template <typename T, int W>
+__host__ __device__ constexpr size_t spmv_tile_smem_bytes(int n_z) {
+    using G = SpmvTile<W>;
+    return sizeof(T) * (4 * static_cast<size_t>(n_z) + static_cast<size_t>(G::NS) * 3 * G::NT +
+                        static_cast<size_t>(G::NS) * G::N);
+}
+
+template <typename T, bool Fast, int W, int D>
+__global__ void __launch_bounds__(32 * W)
+    k_fused_spmv_tile(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
+                      T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
+                      const Scalars<T>* __restrict__ S) {
+    using A = Ar<T, Fast>;
+    using G = SpmvTile<W>;
+    constexpr int NT = G::NT, NS = G::NS, CW = G::CW, TN = G::N;
+    static_assert(D >= 1 && D <= NS - 2, "the tile of level k+D+1 reuses the slot of level k-1");
+    static_assert(W >= 4 && W + 2 <= 32, "four warps load the halo");
+    if (S->done) return;  // block-uniform
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int lane = threadIdx.x, w = threadIdx.y;
+    const int tid = w * 32 + lane;
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);
+    T* ring = prof + 4 * n_z + tid;  // [slot][3][NT]: p, q, u
+    T* tile = prof + 4 * n_z + NS * 3 * NT;  // [slot][R][CW]
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+
+    const int j0 = blockIdx.x * 32, il0 = blockIdx.y * W;
+    const int j = j0 + lane, il = il0 + w;
+    const bool valid = j < m && il < v.m_loc;
+    const int jc = j < m ? j : m - 1;
+    const int ilc = il < v.m_loc ? il : v.m_loc - 1;
+    const Col<T> c = load_col(v, ilc, jc);
+    // tile coordinates of this column and of its four neighbours (a missing
+    // neighbour reads the column's own value with coefficient 0, operator.hpp:85-92)
+    const int own = (w + 1) * CW + lane + 1;
+    const int oe = c.oe != 0 ? CW : 0, ow = c.ow != 0 ? -CW : 0;
+    const int on = c.on != 0 ? 1 : 0, os = c.os != 0 ? -1 : 0;
+    // tile loads: every thread copies the value at its own tile position; warps
+    // 0/1 also copy halo rows 0 / W+1, warps 2/3 (lanes < W+2) halo columns 0 / 33.
+    // Rows outside the slab clamp to its ghost planes, columns to [0, m).
+    auto gaddr = [&](int rr, int cc) -> const T* {
+        int it = il0 - 1 + rr;
+        it = it < -1 ? -1 : (it > v.m_loc ? v.m_loc : it);
+        int jt = j0 - 1 + cc;
+        jt = jt < 0 ? 0 : (jt >= m ? m - 1 : jt);
+        return z + static_cast<long long>(it) * v.plane + jt;
+    };
+    const T* g0 = gaddr(w + 1, lane + 1);
+    const T* g1 = nullptr;
+    int s1 = 0;
+    if (w == 0) {
+        g1 = gaddr(0, lane + 1);
+        s1 = lane + 1;
+    } else if (w == 1) {
+        g1 = gaddr(W + 1, lane + 1);
+        s1 = (W + 1) * CW + lane + 1;
+    } else if (w == 2 && lane < W + 2) {
+        g1 = gaddr(lane, 0);
+        s1 = lane * CW;
+    } else if (w == 3 && lane < W + 2) {
+        g1 = gaddr(lane, CW - 1);
+        s1 = lane * CW + CW - 1;
+    }
+    const long long base = static_cast<long long>(ilc) * v.plane + jc;
+    T* uc = u + base;
+    T* pc = p + base;
+    T* qc = q + base;
+    const long long sm = m;
+
+    auto issue_tile = [&](int kk, int slot) {  // z tile of level kk into tile slot
+        T* ts = tile + slot * TN;
+        cpa(ts + own, g0 + kk * sm);
+        if (g1) cpa(ts + s1, g1 + kk * sm);
+    };
+    auto issue = [&](int kk, int slot) {  // level kk: p, q, u and the z tile of kk+1
+        cpa(ring + (3 * slot + 0) * NT, pc + kk * sm);
+        cpa(ring + (3 * slot + 1) * NT, qc + kk * sm);
+        cpa(ring + (3 * slot + 2) * NT, uc + kk * sm);
+        if (kk + 1 < n_z) issue_tile(kk + 1, (slot + 1) & (NS - 1));
+    };
+    issue_tile(0, 0);
+    cp_commit();
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        if (t < n_z) issue(t, t);
+        cp_commit();
+    }
+    __syncthreads();  // profile
+    const T alpha = S->alpha, beta = S->beta;
+    T zd = T(0), sig = T(0);
+    for (int kg = 0; kg < n_z; kg += NS) {
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const int k = kg + t;
+            if (k < n_z) {  // block-uniform
+                cp_wait<D - 1>();
+                __syncthreads();
+                const T* ts = tile + t * TN;
+                const T z0 = ts[own];
+                if (k == 0) zd = z0;
+                const T zu = k + 1 < n_z ? tile[((t + 1) & (NS - 1)) * TN + own] : z0;
+                const T ze = ts[own + oe], zw = ts[own + ow], zn = ts[own + on], zs = ts[own + os];
+                T pv = ring[(3 * t + 0) * NT], qv = ring[(3 * t + 1) * NT];
+                const T uv = ring[(3 * t + 2) * NT];
+                if (k + D < n_z) issue(k + D, (t + D) & (NS - 1));
+                cp_commit();
+                const long long l = static_cast<long long>(k) * sm;
+                const T un = A::add(uv, A::mul(alpha, pv));
+                pv = A::add(A::mul(beta, pv), z0);
+                qv = A::mul(beta, qv);
+                const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw,
+                                              c.an, c.as, z0, zu, zd, ze, zw, zn, zs);
+                qv = A::add(qv, A::mul(dP[k], dq));
+                sig = A::add(sig, A::mul(pv, qv));
+                if (valid) {
+                    __stcs(uc + l, un);
+                    __stcs(pc + l, pv);
+                    __stcs(qc + l, qv);
+                }
+                zd = z0;
+            }
+        }
+    }
+    cp_wait<0>();
+    if (valid) part[static_cast<long long>(il) * m + j] = sig;
+}

@@ -279,3 +279,47 @@ def test_device_resident_capi(acg):
     r = s.finish()
     uo, ro = o.solve(o.random_field(42), epsilon=1e-300, maxiter=10)
     assert np.array_equal(r["residual_history"], ro.residual_history)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("m,n_z", [(33, 20), (64, 128), (32, 3), (8, 9)])
+def test_thomas_special_values_bit_exact(acg, dtype, m, n_z):
+    """Zero, denormal, tiny and huge residuals fail the TMEM sweep's numerator
+    range checks; those level groups are recomputed with the reference's own
+    divisions, so both sweeps stay bit-identical (acg_thomas_tm.cuh)."""
+    prob = Problem(m, n_z)
+    o = Oracle(prob)
+    ctx = ctx_for(acg, prob, dtype)
+    assert ctx.info["thomas_tmem"]
+    f32 = dtype == np.float32
+    x = o.random_field(5, dtype)
+    x[::3, :, 1:3] = 0.0
+    x[1::5, :, n_z // 2] = np.finfo(dtype).tiny / 4  # denormal
+    x[2::7, ::2, :] *= np.float32(1e-25) if f32 else 1e-200
+    x[3::11, 1::3, :] *= np.float32(1e12) if f32 else 1e150
+    assert np.array_equal(acg.precondition(ctx, x), o.precondition(x))
+    q = o.random_field(105, dtype)
+    for alpha in (0.0, 0.37):
+        gr, gz, grn, gk = acg.interleaved_prec_kernel(ctx, x, q, alpha)
+        orr, oz, orn, ok, _, _ = o.fused_prec(x, q, alpha)
+        assert np.array_equal(gr, orr) and np.array_equal(gz, oz)
+        assert grn == orn and gk == ok
+
+
+def test_thomas_fallback_when_ranges_fail(acg):
+    """A context whose divisors leave the validated ranges (|T| d_k < 2^-400)
+    keeps the global-memory sweep (k_thomas) and is still bit-identical."""
+    from paper_1302_7193_b200 import capi
+    prob = Problem(16, 24)
+    o = Oracle(prob)
+    o.d = o.d * 1e-150
+    o._build()
+    ctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag)
+    assert not ctx.info()["thomas_tmem"]
+    g = Oracle(prob)
+    good = capi.Context(g.ap, g.bp, g.cp, g.d, g.area, g.east, g.north, g.diag)
+    assert good.info()["thomas_tmem"]
+    x = o.random_field(5)
+    xf, yf = ctx.field().upload(x), ctx.field()
+    capi.precondition(ctx, xf, yf)
+    assert np.array_equal(yf.download(), o.precondition(x))
