@@ -104,9 +104,12 @@ size_t thomas_smem_per_block(int dsize, int n_z, bool global_phi);
 // ----------------------------------------------------------------- launchers
 extern long long g_launches;  // kernel launches issued (all entry points)
 
+// The fused sweeps return the number of reduction-tree leaves they wrote to
+// `stage` (cta_subtree_sums; stage == nullptr or 0: per-column partials were
+// written to part_* and the reduction runs k_tree1).
 template <typename T>
-void launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                       T* part_k, Scalars<T>* S, T* phi_scratch, cudaStream_t st);
+int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st);
 // Once per slab: may the sweeps use the TMEM kernel with common-path
 // divisions (k_validate_tm)? Synchronous.
 template <typename T>
@@ -115,8 +118,8 @@ template <typename T>
 void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scalars<T>* S,
                          const Scalars<T>* gate, T* phi_scratch, cudaStream_t st);
 template <typename T>
-void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                       const Scalars<T>* S, cudaStream_t st);
+int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
+                      const Scalars<T>* S, T* stage, cudaStream_t st);
 template <typename T>
 void launch_apply(const SlabView<T>& v, bool fast, const T* x, T* y, const Scalars<T>* gate,
                   cudaStream_t st);

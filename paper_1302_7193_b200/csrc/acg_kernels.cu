@@ -116,6 +116,35 @@ __device__ __forceinline__ Col<T> load_col(const SlabView<T>& v, int il, int j) 
     return s;
 }
 
+// Stage 1 of the reduction fused into a sweep's epilogue. When a CTA's NT
+// columns are one aligned node of the reference's tree over the slab's column
+// order (slab column count a power of two, CTA = NT consecutive columns of one
+// i-plane), that node is a perfect binary tree over NT/8 sequential sums of 8
+// (parallel.hpp:11-20: n <= 8 sequential, else split in halves). vals[a][col]
+// holds the CTA's per-column partials in column order; warp 0 reduces them and
+// writes stage[a * nleaves + leaf], exactly the value k_tree1 would produce
+// for that node. Requires nv * NT / 8 <= 32.
+template <typename T, int NT>
+__device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __restrict__ stage,
+                                                 int nleaves, long long leaf) {
+    constexpr int B = NT / 8;  // sequential blocks per array
+    static_assert(B >= 1 && B <= 32 && (B & (B - 1)) == 0, "power-of-two block count");
+    const int lane = threadIdx.x;
+    const int a = lane / B, b = lane % B;
+    T v = T(0);
+    if (a < nv) {
+        const T* x = vals + a * NT + 8 * b;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) v = add_rn(v, x[l]);
+    }
+#pragma unroll
+    for (int w = 1; w < B; w <<= 1) {
+        const T o = __shfl_down_sync(0xffffffffu, v, w, B);
+        if (b % (2 * w) == 0) v = add_rn(v, o);
+    }
+    if (a < nv && b == 0) stage[a * static_cast<long long>(nleaves) + leaf] = v;
+}
+
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
 #include "acg_thomas_tm.cuh"
@@ -184,7 +213,7 @@ template <typename T, bool Fast, int X = 1>
 __global__ void __launch_bounds__(32 * kStencilWarps)
     k_fused_spmv_ring(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                      const Scalars<T>* __restrict__ S) {
+                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
     using A = Ar<T, Fast>;
     constexpr int NT = 32 * kStencilWarps, D = kSpmvD, NS = kSpmvD + 1;
     if (S->done) return;
@@ -258,6 +287,15 @@ __global__ void __launch_bounds__(32 * kStencilWarps)
         z0 = zu;
     }
     cp_wait<0>();
+    if (stage != nullptr) {  // fused reduction stage 1 (X = 8: one plane x 256 j, all valid)
+        __syncthreads();
+        ring[tid] = sig;
+        __syncthreads();
+        if (threadIdx.y == 0)
+            cta_subtree_sums<T, NT>(ring, 1, stage, nleaves,
+                                    (static_cast<long long>(il) * m + blockIdx.x * NT) / NT);
+        return;
+    }
     part[static_cast<long long>(il) * m + j] = sig;
 }
 
@@ -766,20 +804,36 @@ inline int thomas_choice() {
         const char* e = std::getenv("ACG_THOMAS");
         if (!e) return 0;
         const std::string s(e);
-        const char* names[] = {"", "2,4,7", "4,4,7", "2,8,7", "4,8,7", "2,2,7", "4,4,5", "8,4,7", "4,2,7", "8,2,7"};
-        for (int a = 1; a < 10; ++a)
+        const char* names[] = {"", "2,4,7", "4,4,7"};
+        for (int a = 1; a < 3; ++a)
             if (s == names[a]) return a;
         return 0;
     }();
     return c;
 }
 
+// Leaves of the reduction tree a sweep can emit directly (cta_subtree_sums):
+// CTAs of `cols` consecutive columns of one i-plane, slab column count a power
+// of two (so every CTA is an aligned node), at most 16384 leaves (k_tree2).
+// 0: the sweep writes per-column partials and k_tree1 runs instead.
+template <typename T>
+int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
+    static const bool off = [] {
+        const char* e = std::getenv("ACG_FUSED_REDUCE");
+        return e && std::string(e) == "0";
+    }();
+    if (off || stage == nullptr || cols <= 0 || v.m % cols != 0) return 0;
+    const long long ncol = static_cast<long long>(v.m_loc) * v.m;
+    if ((ncol & (ncol - 1)) != 0 || ncol / cols > 16384 || ncol / cols < 1) return 0;
+    return static_cast<int>(ncol / cols);
+}
+
 // TMEM-resident sweep (k_thomas_tm). Shared memory is padded so that no more
 // CTAs become resident on an SM than its 512 TMEM columns can serve (a CTA
 // beyond that would only wait inside tcgen05.alloc).
 template <typename T, bool Fast, bool Fused, class C>
-void launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
-                          Scalars<T>* S, const Scalars<T>* gate, cudaStream_t st) {
+int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
+                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
     const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
     const dim3 block(32, C::W);
     constexpr int PW = C::W / C::X;  // i-planes per CTA
@@ -788,8 +842,12 @@ void launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
     const size_t max_ctas = 512u / tcols;
     const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
     if (smem < floor_bytes) smem = floor_bytes;
+    // fused stage 1: CTA = one aligned node (128 consecutive columns) of the tree
+    const int leaves = fused_leaves(v, C::X == 4 ? C::NT : 0, Fused ? stage : nullptr);
     ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
-    k_thomas_tm<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, tcols);
+    k_thomas_tm<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, tcols,
+                                                             leaves ? stage : nullptr, leaves);
+    return leaves;
 }
 
 // ACG_THOMAS_TM="CP,D,DB" selects a compiled TMEM configuration; "0" disables
@@ -799,8 +857,8 @@ inline int thomas_tm_choice() {
         const char* e = std::getenv("ACG_THOMAS_TM");
         if (!e) return 1;
         const std::string s(e);
-        const char* names[] = {"0", "4,15,15", "4,15,15,1", "4,15,15,2", "8,15,15", "4,12,12", "2,15,15", "4,15,8"};
-        for (int a = 0; a < 8; ++a)
+        const char* names[] = {"0", "4,15,15", "4,15,15,1", "8,15,15", "2,15,15"};
+        for (int a = 0; a < 5; ++a)
             if (s == names[a]) return a;
         return 1;
     }();
@@ -808,37 +866,27 @@ inline int thomas_tm_choice() {
 }
 
 template <typename T, bool Fast, bool Fused>
-void launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
-                   const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
+int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
+                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
     const int tmc = thomas_tm_choice();
     if (tmc != 0 && v.tm_ok && phi_scratch == nullptr && thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
-#define ACG_TM(...) launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, st)
+#define ACG_TM(...) return launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, stage, st)
         switch (tmc) {
-            case 2: ACG_TM(ThomasTmCfg<4, 15, 15, 1>); break;
-            case 3: ACG_TM(ThomasTmCfg<4, 15, 15, 2>); break;
-            case 4: ACG_TM(ThomasTmCfg<8, 15, 15>); break;
-            case 5: ACG_TM(ThomasTmCfg<4, 12, 12>); break;
-            case 6: ACG_TM(ThomasTmCfg<2, 15, 15>); break;
-            case 7: ACG_TM(ThomasTmCfg<4, 15, 8>); break;
-            default: ACG_TM(ThomasTmCfg<4, 15, 15>); break;
+            case 2: ACG_TM(ThomasTmCfg<4, 15, 15, 1>);
+            case 3: ACG_TM(ThomasTmCfg<8, 15, 15>);
+            case 4: ACG_TM(ThomasTmCfg<2, 15, 15>);
+            default: ACG_TM(ThomasTmCfg<4, 15, 15>);
         }
 #undef ACG_TM
-        return;
     }
 #define ACG_TH(...) launch_thomas_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, phi_scratch, st)
     switch (thomas_choice()) {
         case 1: ACG_TH(ThomasCfg<2, 4, 7>); break;
         case 2: ACG_TH(ThomasCfg<4, 4, 7>); break;
-        case 3: ACG_TH(ThomasCfg<2, 8, 7>); break;
-        case 4: ACG_TH(ThomasCfg<4, 8, 7>); break;
-        case 5: ACG_TH(ThomasCfg<2, 2, 7>); break;
-        case 6: ACG_TH(ThomasCfg<4, 4, 5>); break;
-        case 7: ACG_TH(ThomasCfg<8, 4, 7>); break;
-        case 8: ACG_TH(ThomasCfg<4, 2, 7>); break;
-        case 9: ACG_TH(ThomasCfg<8, 2, 7>); break;
         default: ACG_TH(typename ThomasOf<T>::type); break;
     }
 #undef ACG_TH
+    return 0;
 }
 
 }  // namespace
@@ -876,28 +924,33 @@ bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st) {
 }
 
 template <typename T>
-void launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                       T* part_k, Scalars<T>* S, T* phi_scratch, cudaStream_t st) {
-    if (fast)
-        launch_thomas<T, true, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch, st);
-    else
-        launch_thomas<T, false, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch, st);
+int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st) {
+    const int leaves =
+        fast ? launch_thomas<T, true, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
+                                            stage, st)
+             : launch_thomas<T, false, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
+                                             stage, st);
     post_launch("fused_prec");
+    return leaves;
 }
 
 template <typename T>
 void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scalars<T>* S,
                          const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
     if (fast)
-        launch_thomas<T, true, false>(v, nullptr, y, x, nullptr, nullptr, S, gate, phi_scratch, st);
+        launch_thomas<T, true, false>(v, nullptr, y, x, nullptr, nullptr, S, gate, phi_scratch,
+                                      nullptr, st);
     else
-        launch_thomas<T, false, false>(v, nullptr, y, x, nullptr, nullptr, S, gate, phi_scratch, st);
+        launch_thomas<T, false, false>(v, nullptr, y, x, nullptr, nullptr, S, gate, phi_scratch,
+                                       nullptr, st);
     post_launch("precondition");
 }
 
 template <typename T>
-void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                       const Scalars<T>* S, cudaStream_t st) {
+int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
+                      const Scalars<T>* S, T* stage, cudaStream_t st) {
+    int leaves = 0;
     const dim3 block(32, kStencilWarps);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
     // ACG_SPMV=plain|ring|tile overrides the variant; ACG_SPMV_D the tile prefetch depth,
@@ -926,16 +979,21 @@ void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const 
     } else if (mode == 2) {
         const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                          static_cast<size_t>(kSpmvD + 1) * 4 * 32 * kStencilWarps);
-        static const int X = [] {
+        // X: warps along j, the widest contiguous row chunk m allows (env override)
+        static const int Xenv = [] {
             const char* e = std::getenv("ACG_SPMV_X");
-            return e ? std::atoi(e) : 8;
+            return e ? std::atoi(e) : 0;
         }();
+        const int X = Xenv ? Xenv
+                           : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
+        if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
+        T* stg = leaves ? stage : nullptr;
 #define ACG_RX(F, XX)                                                                             \
     do {                                                                                          \
         const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
                       (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
         ensure_smem(k_fused_spmv_ring<T, F, XX>, smem);                                           \
-        k_fused_spmv_ring<T, F, XX><<<g2, block, smem, st>>>(v, u, p, q, z, part, S);             \
+        k_fused_spmv_ring<T, F, XX><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
     } while (0)
         if (fast) {
             if (X == 2) ACG_RX(true, 2); else if (X == 4) ACG_RX(true, 4); else if (X == 8) ACG_RX(true, 8); else ACG_RX(true, 1);
@@ -958,6 +1016,7 @@ void launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const 
 #undef ACG_SP
     }
     post_launch("fused_spmv");
+    return leaves;
 }
 
 template <typename T>
@@ -1071,12 +1130,12 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
 
 #define ACG_INSTANTIATE(T)                                                                      \
     template bool validate_thomas_tm<T>(const SlabView<T>&, cudaStream_t);                      \
-    template void launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,      \
-                                       Scalars<T>*, T*, cudaStream_t);                          \
+    template int launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,       \
+                                      Scalars<T>*, T*, T*, cudaStream_t);                       \
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
                                          const Scalars<T>*, T*, cudaStream_t);                  \
-    template void launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,      \
-                                       const Scalars<T>*, cudaStream_t);                        \
+    template int launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,       \
+                                      const Scalars<T>*, T*, cudaStream_t);                     \
     template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \
                                   cudaStream_t);                                                \
     template void launch_residual_partials<T>(const SlabView<T>&, bool, const T*, const T*, T*, \

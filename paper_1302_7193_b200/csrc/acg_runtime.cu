@@ -448,7 +448,8 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
             if (s.plan.blocks > 16384)
                 fail(ACG_ERR_INVALID_ARGUMENT, "slab of %lld columns exceeds the reduction plan",
                      ncol);
-            CK(cudaMalloc(&s.stage, 3 * static_cast<size_t>(s.plan.blocks) * c->s));
+            // stage: k_tree1 block sums, or up to 16384 node sums written by a sweep
+            CK(cudaMalloc(&s.stage, 3 * static_cast<size_t>(std::max(s.plan.blocks, 16384)) * c->s));
             if (thomas_smem_per_block(static_cast<int>(c->s), d->n_z, false) > 200 * 1024)
                 CK(cudaMalloc(&s.phi, s.n_loc * c->s));  // tall columns: phi in HBM
         }
@@ -686,20 +687,28 @@ void halo(const acg_context* c, const acg_field* f) {
 // -------------------------------------------------------------- reductions
 // Reduce nv per-column partial arrays of every local slab (already written to
 // slab.part[0..nv)) and run scalar program `op` on every slab's Scalars.
+// leaves[si] > 0: the sweep already wrote that many aligned tree-node sums to
+// slab.stage (fused stage 1), so only the perfect tree above them remains.
 template <typename T>
 void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>& S,
-            const Scalars<T>* gate_or_null, bool gated) {
+            const Scalars<T>* gate_or_null, bool gated, const std::vector<int>* leaves = nullptr) {
     const bool single = c->nslabs_total == 1;
     T* gather = static_cast<T*>(c->gather);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& s = c->slabs[si];
         const Scalars<T>* gate = gated ? (gate_or_null ? gate_or_null : S[si]) : nullptr;
-        launch_tree_stage1<T>(s.plan, static_cast<const T*>(s.part[0]),
-                              static_cast<const T*>(s.part[1]), static_cast<const T*>(s.part[2]),
-                              nv, static_cast<T*>(s.stage), gate, c->stream);
+        TreePlan plan = s.plan;
+        if (leaves && (*leaves)[si] > 0) {
+            plan.blocks = (*leaves)[si];
+        } else {
+            launch_tree_stage1<T>(s.plan, static_cast<const T*>(s.part[0]),
+                                  static_cast<const T*>(s.part[1]),
+                                  static_cast<const T*>(s.part[2]), nv,
+                                  static_cast<T*>(s.stage), gate, c->stream);
+        }
         T* g = c->comm ? static_cast<T*>(c->gather_send) : gather;
         const int slot = c->comm ? 0 : s.index;
-        launch_tree_stage2<T>(s.plan, static_cast<const T*>(s.stage), nv, g, slot, single,
+        launch_tree_stage2<T>(plan, static_cast<const T*>(s.stage), nv, g, slot, single,
                               c->nslabs_total, c->exact_tree, S[si], op, c->stream);
     }
     if (single) return;
@@ -1009,12 +1018,14 @@ acg_status acg_interleaved_spmv_kernel(const acg_context* c, acg_field* u, acg_f
             reset_tmp<T>(c, static_cast<T>(alpha), static_cast<T>(beta));
             auto S = tmp_scalars<T>(c);
             halo(c, z);
+            std::vector<int> leaves(c->slabs.size());
             for (size_t si = 0; si < c->slabs.size(); ++si)
-                launch_fused_spmv<T>(view<T>(c, si), c->fast(), static_cast<T*>(u->data(si)),
-                                     static_cast<T*>(p->data(si)), static_cast<T*>(q->data(si)),
-                                     static_cast<const T*>(z->data(si)),
-                                     static_cast<T*>(c->slabs[si].part[0]), S[si], c->stream);
-            reduce<T>(c, 1, kOpStore, S, nullptr, false);
+                leaves[si] = launch_fused_spmv<T>(
+                    view<T>(c, si), c->fast(), static_cast<T*>(u->data(si)),
+                    static_cast<T*>(p->data(si)), static_cast<T*>(q->data(si)),
+                    static_cast<const T*>(z->data(si)), static_cast<T*>(c->slabs[si].part[0]),
+                    S[si], static_cast<T*>(c->slabs[si].stage), c->stream);
+            reduce<T>(c, 1, kOpStore, S, nullptr, false, &leaves);
             const Scalars<T> h = read_scalars<T>(c, S[0]);
             if (sigma) *sigma = static_cast<double>(h.val[0]);
         });
@@ -1033,18 +1044,20 @@ acg_status acg_interleaved_prec_kernel(const acg_context* c, acg_field* r, acg_f
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c, static_cast<T>(alpha));
             auto S = tmp_scalars<T>(c);
+            std::vector<int> leaves(c->slabs.size());
             for (size_t si = 0; si < c->slabs.size(); ++si) {
                 const Slab& s = c->slabs[si];
-                launch_fused_prec<T>(view<T>(c, si), c->fast(), static_cast<T*>(r->data(si)),
-                                     static_cast<T*>(z->data(si)), static_cast<const T*>(q->data(si)),
-                                     static_cast<T*>(s.part[0]), static_cast<T*>(s.part[1]), S[si],
-                                     static_cast<T*>(s.phi), c->stream);
+                leaves[si] = launch_fused_prec<T>(
+                    view<T>(c, si), c->fast(), static_cast<T*>(r->data(si)),
+                    static_cast<T*>(z->data(si)), static_cast<const T*>(q->data(si)),
+                    static_cast<T*>(s.part[0]), static_cast<T*>(s.part[1]), S[si],
+                    static_cast<T*>(s.phi), static_cast<T*>(s.stage), c->stream);
             }
             for (Scalars<T>* s : S)
                 if (read_scalars<T>(c, s).pivot)
                     fail(ACG_ERR_BREAKDOWN,
                          "interleaved_prec_kernel: zero pivot in tridiagonal elimination");
-            reduce<T>(c, 2, kOpStore, S, nullptr, false);
+            reduce<T>(c, 2, kOpStore, S, nullptr, false, &leaves);
             const Scalars<T> h = read_scalars<T>(c, S[0]);
             if (r_norm) *r_norm = static_cast<double>(std::sqrt(h.val[0]));
             if (kappa) *kappa = static_cast<double>(h.val[1]);
@@ -1131,6 +1144,7 @@ struct acg_solver {
     long long launches0 = 0;
     EventTimer timer;       // per-family timings (record_timings)
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
+    std::vector<int> leaves;  // per slab: tree leaves the last sweep wrote (fused stage 1)
     std::chrono::steady_clock::time_point t0;
     ~acg_solver() {
         for (acg_field* fl : {u, r, z, p, q})
@@ -1286,29 +1300,33 @@ template <typename T>
 void iterate_interleaved(acg_solver* s) {
     const acg_context* c = s->ctx;
     auto S = sv<T>(s);
+    std::vector<int>& leaves = s->leaves;
+    leaves.resize(c->slabs.size());
     s->timer.begin(kFusedPrec);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& sl = c->slabs[si];
         s->ktimer.begin(kFusedPrec);
-        launch_fused_prec<T>(view<T>(c, si), c->fast(), static_cast<T*>(s->r->data(si)),
-                             static_cast<T*>(s->z->data(si)), static_cast<const T*>(s->q->data(si)),
-                             static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), S[si],
-                             static_cast<T*>(sl.phi), c->stream);
+        leaves[si] = launch_fused_prec<T>(
+            view<T>(c, si), c->fast(), static_cast<T*>(s->r->data(si)),
+            static_cast<T*>(s->z->data(si)), static_cast<const T*>(s->q->data(si)),
+            static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), S[si],
+            static_cast<T*>(sl.phi), static_cast<T*>(sl.stage), c->stream);
         s->ktimer.end(kFusedPrec);
     }
-    reduce<T>(c, 2, kOpIlPrec, S, nullptr, true);
+    reduce<T>(c, 2, kOpIlPrec, S, nullptr, true, &leaves);
     s->timer.end(kFusedPrec);
     s->timer.begin(kFusedSpmv);
     halo(c, s->z);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         s->ktimer.begin(kFusedSpmv);
-        launch_fused_spmv<T>(view<T>(c, si), c->fast(), static_cast<T*>(s->u->data(si)),
-                             static_cast<T*>(s->p->data(si)), static_cast<T*>(s->q->data(si)),
-                             static_cast<const T*>(s->z->data(si)),
-                             static_cast<T*>(c->slabs[si].part[0]), S[si], c->stream);
+        leaves[si] = launch_fused_spmv<T>(
+            view<T>(c, si), c->fast(), static_cast<T*>(s->u->data(si)),
+            static_cast<T*>(s->p->data(si)), static_cast<T*>(s->q->data(si)),
+            static_cast<const T*>(s->z->data(si)), static_cast<T*>(c->slabs[si].part[0]), S[si],
+            static_cast<T*>(c->slabs[si].stage), c->stream);
         s->ktimer.end(kFusedSpmv);
     }
-    reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true);
+    reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true, &leaves);
     s->timer.end(kFusedSpmv);
 }
 

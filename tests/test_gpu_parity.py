@@ -323,3 +323,25 @@ def test_thomas_fallback_when_ranges_fail(acg):
     xf, yf = ctx.field().upload(x), ctx.field()
     capi.precondition(ctx, xf, yf)
     assert np.array_equal(yf.download(), o.precondition(x))
+
+
+@pytest.mark.parametrize("m,n_z", [(256, 6), (512, 3)])
+def test_fused_reduction_stage_bit_exact(acg, m, n_z):
+    """Power-of-two panels whose rows fill whole CTAs: both sweeps emit the
+    reduction tree's node sums from their epilogue (cta_subtree_sums) instead of
+    per-column partials; norms, kappa, sigma and a short solve stay bit-exact."""
+    prob = Problem(m, n_z)
+    o = Oracle(prob)
+    ctx = ctx_for(acg, prob)
+    u, p, q, z = (o.random_field(s) for s in (101, 104, 105, 103))
+    gu, gp, gq, gs = acg.interleaved_spmv_kernel(ctx, u, p, q, z, 0.37, 0.21)
+    ou, op, oq, osg, _ = o.fused_spmv(u, p, q, z, 0.37, 0.21)
+    assert np.array_equal(gq, oq) and gs == osg
+    r = o.random_field(102)
+    gr, gz, grn, gk = acg.interleaved_prec_kernel(ctx, r, q, 0.37)
+    orr, oz, orn, ok, _, _ = o.fused_prec(r, q, 0.37)
+    assert np.array_equal(gz, oz) and grn == orn and gk == ok
+    f = o.random_field(42)
+    ug, rg, uo, ro = _solve_both(acg, o, ctx, f, 0, epsilon=1e-300, maxiter=6)
+    assert _same_result(rg, ro)
+    assert np.array_equal(ug, uo)
