@@ -62,7 +62,9 @@ def algorithmic_bytes(cfg, s):
     m, n_z = cfg["m"], cfg["n_z"]
     N = m * m * n_z
     return {"fused_prec": s * (4 * N + 2 * m * m), "fused_spmv": s * (7 * N + 6 * m * m),
-            "iteration": s * (11 * N + 8 * m * m)}
+            "iteration": s * (11 * N + 8 * m * m),
+            # unfused (standard) loop: apply 2, precondition 2, BLAS-1 16 refs
+            "iteration_standard": s * (20 * N + 8 * m * m)}
 
 
 def peaks():
@@ -272,7 +274,7 @@ def run_gpu(args, cfg):
     nd, td = (n2, t2) if dom == "fused_spmv" else (n1, t1)
     per_launch_ms = td / max(nd, 1)
     bytes_launch = ab[dom] * local_frac
-    achieved = bytes_launch / (per_launch_ms * 1e-3) / 1e9
+    achieved = bytes_launch / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
@@ -286,9 +288,14 @@ def run_gpu(args, cfg):
             "algorithmic_bytes_per_launch": bytes_launch, "peak_kind": pk_kind,
             "launch_ms": per_launch_ms,
             "fused_prec_ms": t1 / max(n1, 1), "fused_spmv_ms": t2 / max(n2, 1),
-            "fused_prec_gbs": ab["fused_prec"] * local_frac / (t1 / max(n1, 1) * 1e-3) / 1e9,
-            "fused_spmv_gbs": ab["fused_spmv"] * local_frac / (t2 / max(n2, 1) * 1e-3) / 1e9}
-    iter_gbs = ab["iteration"] * it_s / 1e9
+            "fused_prec_gbs": ab["fused_prec"] * local_frac / (t1 / n1 * 1e-3) / 1e9 if n1 and t1 else None,
+            "fused_spmv_gbs": ab["fused_spmv"] * local_frac / (t2 / n2 * 1e-3) / 1e9 if n2 and t2 else None}
+    iter_bytes = ab["iteration_standard" if args.variant == "standard" else "iteration"]
+    iter_gbs = iter_bytes * it_s / 1e9
+    if args.variant == "standard":  # no K1/K2 launches: roofline at the iteration level
+        roof.update({"kernel": "iteration (standard loop, 9 sweeps)", "achieved": iter_gbs,
+                     "frac": iter_gbs / pk["hbm_gbs"], "traffic": None,
+                     "algorithmic_bytes_per_launch": iter_bytes, "launch_ms": ms_max / args.steps})
 
     # ---- e2e through the C ABI with pinned host buffers (H2D f, solve, D2H u)
     e2e = None
@@ -302,14 +309,16 @@ def run_gpu(args, cfg):
         f2, u2 = ctx.field(), ctx.field()
         # one untimed warm-up call (allocates the context's cached solver state)
         f2.upload(hf.array, scope=capi.HOST_LOCAL)
-        capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps)
+        capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps,
+                         variant=variant)
         u2.download(out=hu.array, scope=capi.HOST_LOCAL)
         barrier()
         t0 = time.perf_counter()
         f2.upload(hf.array, scope=capi.HOST_LOCAL)
         ctx.sync()
         t1 = time.perf_counter()
-        r2 = capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps)
+        r2 = capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps,
+                         variant=variant)
         t2 = time.perf_counter()
         u2.download(out=hu.array, scope=capi.HOST_LOCAL)
         barrier()
@@ -351,7 +360,7 @@ def run_gpu(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic", "config": workload(cfg, args, world),
-            "achieved_gbs_iteration": iter_gbs,
+            "achieved_gbs_iteration": iter_gbs, "algorithmic_bytes_iteration": iter_bytes,
             "frac_of_peak_iteration": iter_gbs / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_timed, "clocks": clk.summary(),
@@ -370,7 +379,7 @@ def run_gpu(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)  # the reference bench protocol (main.cpp:210-217)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))

@@ -961,6 +961,7 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         if (e && std::string(e) == "plain") return 1;
         if (e && std::string(e) == "ring") return 2;
         if (e && std::string(e) == "tile") return 0;
+        if (e && std::string(e) == "ring2") return 3;
         return sizeof(T) == 4 ? 0 : 2;
     }();
     static const int tile_d = [] {
@@ -976,6 +977,29 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             ensure_smem(k_fused_spmv<T, false>, smem);
             k_fused_spmv<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
         }
+    } else if (mode == 3) {
+        static const int Xenv = [] {
+            const char* e = std::getenv("ACG_SPMV_X");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int X = Xenv ? Xenv
+                           : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
+        if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
+        T* stg = leaves ? stage : nullptr;
+        const size_t smem = spmv_ring2_smem_bytes<T>(v.n_z);
+#define ACG_R2(F, XX)                                                                             \
+    do {                                                                                          \
+        const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
+                      (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
+        ensure_smem(k_fused_spmv_ring2<T, F, XX, 3>, smem);                                       \
+        k_fused_spmv_ring2<T, F, XX, 3><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
+    } while (0)
+        if (fast) {
+            if (X == 2) ACG_R2(true, 2); else if (X == 4) ACG_R2(true, 4); else if (X == 8) ACG_R2(true, 8); else ACG_R2(true, 1);
+        } else {
+            if (X == 2) ACG_R2(false, 2); else if (X == 4) ACG_R2(false, 4); else if (X == 8) ACG_R2(false, 8); else ACG_R2(false, 1);
+        }
+#undef ACG_R2
     } else if (mode == 2) {
         const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                          static_cast<size_t>(kSpmvD + 1) * 4 * 32 * kStencilWarps);

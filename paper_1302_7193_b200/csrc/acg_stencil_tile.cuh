@@ -149,3 +149,122 @@ __global__ void __launch_bounds__(32 * W)
     cp_wait<0>();
     if (valid) part[static_cast<long long>(il) * m + j] = sig;
 }
+
+// K2, all stencil inputs through the per-thread cp.async ring (fp64 default).
+// ncu on k_fused_spmv_ring: the i+-1 neighbour loads, even issued a level
+// ahead, still held ~1/4 of the warp samples (those rows belong to other
+// CTAs and often come from DRAM). Here every level's p, q, u, z(k+1), the two
+// i-neighbour rows z(i+-1, k) and, for the warp's edge lanes, the j-neighbour
+// beyond the warp are copied D levels ahead; the j+-1 neighbours inside the
+// warp come from the own z row by shuffles. CTA = one i-plane x 32*X j.
+template <typename T, bool Fast, int X, int D>
+__global__ void __launch_bounds__(32 * kStencilWarps)
+    k_fused_spmv_ring2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
+                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
+                       const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
+    using A = Ar<T, Fast>;
+    constexpr int NT = 32 * kStencilWarps, NS = 4, NA = 7;
+    static_assert(D >= 1 && D < NS, "prefetch depth below the ring size");
+    if (S->done) return;  // block-uniform
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int lane = threadIdx.x;
+    const int tid = threadIdx.y * 32 + lane;
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);
+    const int jw = (blockIdx.x * X + threadIdx.y % X) * 32;  // first column of this warp
+    const int jr = jw + lane;
+    const int il = blockIdx.y * (kStencilWarps / X) + threadIdx.y / X;
+    const bool valid = jr < m && il < v.m_loc;
+    const int j = jr < m ? jr : m - 1;
+    const int ilc = il < v.m_loc ? il : v.m_loc - 1;
+    T* ring = prof + 4 * n_z + tid;  // [slot][NA][NT]
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> c = load_col(v, ilc, j);
+    const long long base = static_cast<long long>(ilc) * v.plane + j;
+    const T* zc = z + base;
+    T* uc = u + base;
+    T* pc = p + base;
+    T* qc = q + base;
+    // edge lanes fetch the j-neighbour outside the warp (clamped into the row)
+    const bool edge = lane == 0 || lane == 31;
+    const int je = lane == 0 ? (jw > 0 ? jw - 1 : 0) : (jw + 32 < m ? jw + 32 : m - 1);
+    const T* zedge = z + static_cast<long long>(ilc) * v.plane + je;
+    const long long sm = m;
+    auto issue = [&](int kk, int slot) {
+        T* r0 = ring + slot * NA * NT;
+        const long long l = kk * sm;
+        cpa(r0 + 0 * NT, pc + l);
+        cpa(r0 + 1 * NT, qc + l);
+        cpa(r0 + 2 * NT, uc + l);
+        if (kk + 1 < n_z) cpa(r0 + 3 * NT, zc + l + sm);
+        cpa(r0 + 4 * NT, zc + l + c.oe);
+        cpa(r0 + 5 * NT, zc + l + c.ow);
+        if (edge) cpa(r0 + 6 * NT, zedge + l);
+    };
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        if (t < n_z) issue(t, t);
+        cp_commit();
+    }
+    __syncthreads();  // profile
+    const T alpha = S->alpha, beta = S->beta;
+    T z0 = zc[0], zd = z0, sig = T(0);
+    for (int kg = 0; kg < n_z; kg += NS) {
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const int k = kg + t;
+            if (k < n_z) {  // block-uniform
+                cp_wait<D - 1>();
+                const T* r0 = ring + t * NA * NT;
+                T pv = r0[0], qv = r0[NT];
+                const T uv = r0[2 * NT];
+                const T zu = k + 1 < n_z ? r0[3 * NT] : z0;
+                const T ze = r0[4 * NT], zw = r0[5 * NT];
+                const T zx = edge ? r0[6 * NT] : T(0);
+                if (k + D < n_z) issue(k + D, (t + D) & (NS - 1));
+                cp_commit();
+                T zn = __shfl_down_sync(0xffffffffu, z0, 1);
+                T zs = __shfl_up_sync(0xffffffffu, z0, 1);
+                if (lane == 31) zn = zx;
+                if (lane == 0) zs = zx;
+                if (c.on == 0) zn = z0;  // panel edge: own value, coefficient 0 (operator.hpp:85-92)
+                if (c.os == 0) zs = z0;
+                const long long l = static_cast<long long>(k) * sm;
+                const T un = A::add(uv, A::mul(alpha, pv));
+                pv = A::add(A::mul(beta, pv), z0);
+                qv = A::mul(beta, qv);
+                const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw,
+                                              c.an, c.as, z0, zu, zd, ze, zw, zn, zs);
+                qv = A::add(qv, A::mul(dP[k], dq));
+                sig = A::add(sig, A::mul(pv, qv));
+                if (valid) {
+                    __stcs(uc + l, un);
+                    __stcs(pc + l, pv);
+                    __stcs(qc + l, qv);
+                }
+                zd = z0;
+                z0 = zu;
+            }
+        }
+    }
+    cp_wait<0>();
+    if (stage != nullptr) {  // fused reduction stage 1 (X = 8: one plane x 256 j, all valid)
+        __syncthreads();
+        ring[0] = sig;
+        __syncthreads();
+        if (threadIdx.y == 0)
+            cta_subtree_sums<T, NT>(prof + 4 * n_z, 1, stage, nleaves,
+                                    (static_cast<long long>(il) * m + blockIdx.x * NT) / NT);
+        return;
+    }
+    if (valid) part[static_cast<long long>(il) * m + jr] = sig;
+}
+
+template <typename T>
+__host__ __device__ constexpr size_t spmv_ring2_smem_bytes(int n_z) {
+    return sizeof(T) * (4 * static_cast<size_t>(n_z) + 4 * 7 * static_cast<size_t>(32 * kStencilWarps));
+}
