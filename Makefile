@@ -27,7 +27,7 @@ all: lib py oracle
 lib: $(LIB)
 py: $(PYMOD)
 
-build/acg_kernels.o: $(CSRC)/acg_kernels.cu $(CSRC)/acg_internal.h
+build/acg_kernels.o: $(CSRC)/acg_kernels.cu $(CSRC)/acg_internal.h $(wildcard $(CSRC)/*.cuh)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/ptxas_kernels.log || (cat build/ptxas_kernels.log; false)
 

@@ -18,6 +18,8 @@
 // order (the reference builds with -ffp-contract=off), which makes the GPU
 // bit-identical to the CPU. The FAST path allows FMA contraction and replaces
 // the three divides per Thomas level by one reciprocal.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -148,6 +150,7 @@ __device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __res
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
 #include "acg_thomas_tm.cuh"
+#include "acg_thomas_tma.cuh"
 
 // ================================================================ K2 / K3 / K8
 constexpr int kStencilWarps = 8;
@@ -850,6 +853,68 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     return leaves;
 }
 
+// 2D TMA view of a plane-major field: dim0 = j (m), dim1 = row = plane*n_z + k
+// over the slab's m_loc planes plus its two ghost planes; box = 8 levels x box_j.
+// `data` points at plane 0 (the ghost plane precedes it). false if the driver
+// entry point is unavailable or the rows are not 16-byte aligned.
+template <typename T>
+bool make_field_map(CUtensorMap* map, const SlabView<T>& v, const T* data, int box_j) {
+    static PFN_cuTensorMapEncodeTiled encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }();
+    if (!encode || (static_cast<size_t>(v.m) * sizeof(T)) % 16 != 0) return false;
+    const T* base = data - v.plane;
+    if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(v.m),
+                                static_cast<cuuint64_t>(v.m_loc + 2) * v.n_z};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(v.m) * sizeof(T)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_j), 8};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                  : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                              2, const_cast<T*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// TMA-fed TMEM sweep (k_thomas_tma); returns -1 when the tensor maps cannot be
+// built (the caller then uses k_thomas_tm).
+template <typename T, bool Fast, bool Fused, class C>
+int launch_thomas_tma_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
+                          Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
+    CUtensorMap m0, m1;
+    if (!make_field_map<T>(&m0, v, Fused ? r : in, 32)) return -1;
+    if (Fused && !make_field_map<T>(&m1, v, in, 32)) return -1;
+    if (!Fused) m1 = m0;
+    const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
+    const dim3 block(32, C::W);
+    const dim3 grid((v.m + C::NT - 1) / C::NT, v.m_loc);
+    size_t smem = thomas_tma_smem_bytes<T, C>(v.n_z);
+    const size_t max_ctas = 512u / tcols;
+    const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
+    if (smem < floor_bytes) smem = floor_bytes;
+    const int leaves = fused_leaves(v, C::NT, Fused ? stage : nullptr);
+    ensure_smem(k_thomas_tma<T, Fast, Fused, C>, smem);
+    k_thomas_tma<T, Fast, Fused, C><<<grid, block, smem, st>>>(
+        v, m0, m1, r, in, out, p2, pk, S, gate, tcols, leaves ? stage : nullptr, leaves);
+    return leaves;
+}
+
+inline bool thomas_tma_enabled() {  // ACG_THOMAS_TMA=1 opts in (measured: no faster than k_thomas_tm)
+    static bool on = [] {
+        const char* e = std::getenv("ACG_THOMAS_TMA");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
+
 // ACG_THOMAS_TM="CP,D,DB" selects a compiled TMEM configuration; "0" disables
 // the TMEM sweep (A/B experiments).
 inline int thomas_tm_choice() {
@@ -869,6 +934,12 @@ template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
                   const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
     const int tmc = thomas_tm_choice();
+    if (thomas_tma_enabled() && tmc != 0 && v.tm_ok && phi_scratch == nullptr &&
+        thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
+        const int l = launch_thomas_tma_cfg<T, Fast, Fused, ThomasTmaCfg<4, 3>>(v, r, in, out, p2, pk,
+                                                                               S, gate, stage, st);
+        if (l >= 0) return l;
+    }
     if (tmc != 0 && v.tm_ok && phi_scratch == nullptr && thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
 #define ACG_TM(...) return launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, stage, st)
         switch (tmc) {
