@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -151,6 +152,7 @@ __device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __res
 #include "acg_thomas.cuh"
 #include "acg_thomas_tm.cuh"
 #include "acg_thomas_tma.cuh"
+#include "acg_thomas_tm2.cuh"
 
 // ================================================================ K2 / K3 / K8
 constexpr int kStencilWarps = 8;
@@ -212,13 +214,13 @@ __global__ void __launch_bounds__(32 * kStencilWarps)
 constexpr int kSpmvD = 6;
 
 // X: warps of a CTA along j (X = 1: 8 i-planes x 32 j; X = 8: 1 plane x 256 j).
-template <typename T, bool Fast, int X = 1>
-__global__ void __launch_bounds__(32 * kStencilWarps)
+template <typename T, bool Fast, int X = 1, int D = kSpmvD, int MINB = 1>
+__global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     k_fused_spmv_ring(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
                       const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
     using A = Ar<T, Fast>;
-    constexpr int NT = 32 * kStencilWarps, D = kSpmvD, NS = kSpmvD + 1;
+    constexpr int NT = 32 * kStencilWarps, NS = D + 1;
     if (S->done) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* prof = reinterpret_cast<T*>(smem_raw);
@@ -907,6 +909,44 @@ int launch_thomas_tma_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
     return leaves;
 }
 
+inline int num_sms() {
+    static int n = [] {
+        int dev = 0, c = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+        return c;
+    }();
+    return n;
+}
+
+// Two columns per thread, persistent (k_thomas_tm2); -1 if not applicable.
+template <typename T, bool Fast, bool Fused, class C>
+int launch_thomas_tm2_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
+                          Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
+    const unsigned tcols = 2 * thomas_tm_cols(v.n_z, sizeof(T));
+    if (v.m % 2 != 0 || tcols > 512) return -1;
+    const int per_sm = static_cast<int>(512u / tcols);
+    const int tiles_row = (v.m + C::COLS - 1) / C::COLS;
+    const int ntiles = tiles_row * v.m_loc;
+    const int grid = std::min(ntiles, num_sms() * per_sm);
+    size_t smem = thomas_tm2_smem_bytes<T, C>(v.n_z);
+    const size_t floor_bytes = 233472u / (per_sm + 1) - 1024u + 64u;
+    if (smem < floor_bytes) smem = floor_bytes;
+    const int leaves = fused_leaves(v, C::COLS, Fused ? stage : nullptr);
+    ensure_smem(k_thomas_tm2<T, Fast, Fused, C>, smem);
+    k_thomas_tm2<T, Fast, Fused, C><<<grid, dim3(32, C::W), smem, st>>>(
+        v, r, in, out, p2, pk, S, gate, tcols, leaves ? stage : nullptr, leaves, ntiles, tiles_row);
+    return leaves;
+}
+
+inline int thomas_tm2_choice() {  // ACG_THOMAS_TM2=1 opts in (measured slower: 0.99 vs 0.80 ms)
+    static int c = [] {
+        const char* e = std::getenv("ACG_THOMAS_TM2");
+        return e && std::string(e) == "1" ? 1 : 0;
+    }();
+    return c;
+}
+
 inline bool thomas_tma_enabled() {  // ACG_THOMAS_TMA=1 opts in (measured: no faster than k_thomas_tm)
     static bool on = [] {
         const char* e = std::getenv("ACG_THOMAS_TMA");
@@ -934,6 +974,13 @@ template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
                   const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
     const int tmc = thomas_tm_choice();
+    const int tm2 = thomas_tm2_choice();
+    if (tm2 != 0 && tmc != 0 && v.tm_ok && phi_scratch == nullptr && !thomas_tma_enabled()) {
+        int l = -1;
+        l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Cfg<4, 15, 15>>(v, r, in, out, p2, pk, S,
+                                                                        gate, stage, st);
+        if (l >= 0) return l;
+    }
     if (thomas_tma_enabled() && tmc != 0 && v.tm_ok && phi_scratch == nullptr &&
         thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
         const int l = launch_thomas_tma_cfg<T, Fast, Fused, ThomasTmaCfg<4, 3>>(v, r, in, out, p2, pk,
@@ -1033,6 +1080,7 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         if (e && std::string(e) == "ring") return 2;
         if (e && std::string(e) == "tile") return 0;
         if (e && std::string(e) == "ring2") return 3;
+        if (e && std::string(e) == "ring8") return 4;
         return sizeof(T) == 4 ? 0 : 2;
     }();
     static const int tile_d = [] {
@@ -1048,6 +1096,35 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             ensure_smem(k_fused_spmv<T, false>, smem);
             k_fused_spmv<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
         }
+    } else if (mode == 4) {
+        static const int Xenv = [] {
+            const char* e = std::getenv("ACG_SPMV_X");
+            return e ? std::atoi(e) : 0;
+        }();
+        static const int Denv = [] {
+            const char* e = std::getenv("ACG_SPMV_D");
+            return e ? std::atoi(e) : 6;
+        }();
+        const int X = Xenv ? Xenv
+                           : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
+        if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
+        T* stg = leaves ? stage : nullptr;
+        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) + 8 * 4 * 32 * kStencilWarps);
+#define ACG_R8(F, XX, DD)                                                                         \
+    do {                                                                                          \
+        const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
+                      (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
+        ensure_smem(k_fused_spmv_ring8<T, F, XX, DD>, smem);                                      \
+        k_fused_spmv_ring8<T, F, XX, DD><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
+    } while (0)
+        if (fast) {
+            if (X == 8) ACG_R8(true, 8, 6); else if (X == 4) ACG_R8(true, 4, 6); else if (X == 2) ACG_R8(true, 2, 6); else ACG_R8(true, 1, 6);
+        } else if (X == 8) {
+            if (Denv == 7) ACG_R8(false, 8, 7); else if (Denv == 5) ACG_R8(false, 8, 5); else if (Denv == 4) ACG_R8(false, 8, 4); else ACG_R8(false, 8, 6);
+        } else {
+            if (X == 4) ACG_R8(false, 4, 6); else if (X == 2) ACG_R8(false, 2, 6); else ACG_R8(false, 1, 6);
+        }
+#undef ACG_R8
     } else if (mode == 3) {
         static const int Xenv = [] {
             const char* e = std::getenv("ACG_SPMV_X");
@@ -1072,8 +1149,12 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         }
 #undef ACG_R2
     } else if (mode == 2) {
-        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
-                                         static_cast<size_t>(kSpmvD + 1) * 4 * 32 * kStencilWarps);
+        // ring depth: D levels (or 10*D + min CTAs/SM); measured best at C3:
+        // D = 2 with 4 CTAs (32 warps) per SM, 1.28 vs 1.33 ms for D = 6 with 3
+        static const int Dr = [] {
+            const char* e = std::getenv("ACG_SPMV_D");
+            return e ? std::atoi(e) : 24;
+        }();
         // X: warps along j, the widest contiguous row chunk m allows (env override)
         static const int Xenv = [] {
             const char* e = std::getenv("ACG_SPMV_X");
@@ -1081,21 +1162,43 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         }();
         const int X = Xenv ? Xenv
                            : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
+        // ring depth actually launched (must match the dispatch below)
+        const int Dx = X == 8 && (Dr == 24 || !fast) ? (Dr > 10 ? Dr / 10 : Dr) : kSpmvD;
+        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
+                                         static_cast<size_t>(Dx + 1) * 4 * 32 * kStencilWarps);
         if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
         T* stg = leaves ? stage : nullptr;
-#define ACG_RX(F, XX)                                                                             \
+#define ACG_RXM(F, XX, MB)                                                                        \
     do {                                                                                          \
         const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
                       (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
-        ensure_smem(k_fused_spmv_ring<T, F, XX>, smem);                                           \
-        k_fused_spmv_ring<T, F, XX><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
+        ensure_smem(k_fused_spmv_ring<T, F, XX, DD, MB>, smem);                                   \
+        k_fused_spmv_ring<T, F, XX, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
     } while (0)
-        if (fast) {
+#define ACG_RX(F, XX) ACG_RXM(F, XX, 1)
+        if (fast && X == 8 && Dr == 24) {
+            constexpr int DD = 2;
+            ACG_RXM(true, 8, 4);
+        } else if (fast) {
+            constexpr int DD = kSpmvD;
             if (X == 2) ACG_RX(true, 2); else if (X == 4) ACG_RX(true, 4); else if (X == 8) ACG_RX(true, 8); else ACG_RX(true, 1);
+        } else if (X == 8 && Dr != kSpmvD) {
+            if (Dr == 4) { constexpr int DD = 4; ACG_RX(false, 8); }
+            else if (Dr == 5) { constexpr int DD = 5; ACG_RX(false, 8); }
+            else if (Dr == 2) { constexpr int DD = 2; ACG_RX(false, 8); }
+            else if (Dr == 34) { constexpr int DD = 3; ACG_RXM(false, 8, 4); }
+            else if (Dr == 24) { constexpr int DD = 2; ACG_RXM(false, 8, 4); }
+            else if (Dr == 25) { constexpr int DD = 2; ACG_RXM(false, 8, 5); }
+            else if (Dr == 14) { constexpr int DD = 1; ACG_RXM(false, 8, 4); }
+            else if (Dr == 15) { constexpr int DD = 1; ACG_RXM(false, 8, 5); }
+            else if (Dr == 16) { constexpr int DD = 1; ACG_RXM(false, 8, 6); }
+            else { constexpr int DD = 3; ACG_RX(false, 8); }
         } else {
+            constexpr int DD = kSpmvD;
             if (X == 2) ACG_RX(false, 2); else if (X == 4) ACG_RX(false, 4); else if (X == 8) ACG_RX(false, 8); else ACG_RX(false, 1);
         }
 #undef ACG_RX
+#undef ACG_RXM
     } else {
         const size_t smem = spmv_tile_smem_bytes<T, kStencilWarps>(v.n_z);
 #define ACG_SP(F, DD)                                                                   \

@@ -268,3 +268,98 @@ template <typename T>
 __host__ __device__ constexpr size_t spmv_ring2_smem_bytes(int n_z) {
     return sizeof(T) * (4 * static_cast<size_t>(n_z) + 4 * 7 * static_cast<size_t>(32 * kStencilWarps));
 }
+
+// K2, k_fused_spmv_ring with an 8-slot ring unrolled by 8 (slot offsets are
+// immediates, no modular slot counters) and prefetch depth D <= 7.
+template <typename T, bool Fast, int X, int D>
+__global__ void __launch_bounds__(32 * kStencilWarps)
+    k_fused_spmv_ring8(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
+                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
+                       const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
+    using A = Ar<T, Fast>;
+    constexpr int NT = 32 * kStencilWarps, NS = 8;
+    static_assert(D >= 1 && D < NS, "prefetch depth below the ring size");
+    if (S->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);
+    __syncthreads();
+    const int j = (blockIdx.x * X + threadIdx.y % X) * 32 + threadIdx.x;
+    const int il = blockIdx.y * (kStencilWarps / X) + threadIdx.y / X;
+    if (stage == nullptr && (j >= m || il >= v.m_loc)) return;
+    T* ring = prof + 4 * n_z + tid;  // [slot][4][NT]
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> c = load_col(v, il, j);
+    const T alpha = S->alpha, beta = S->beta;
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    const T* zc = z + base;
+    T* uc = u + base;
+    T* pc = p + base;
+    T* qc = q + base;
+    const long long sm = m;
+    auto issue = [&](int k, int s) {
+        const long long l = static_cast<long long>(k) * sm;
+        T* r0 = ring + s * 4 * NT;
+        cpa(r0, pc + l);
+        cpa(r0 + NT, qc + l);
+        cpa(r0 + 2 * NT, uc + l);
+        if (k + 1 < n_z) cpa(r0 + 3 * NT, zc + l + sm);
+    };
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        if (t < n_z) issue(t, t);
+        cp_commit();
+    }
+    T z0 = zc[0], zd = z0, sig = T(0);
+    T ze = zc[c.oe], zw = zc[c.ow], zn = zc[c.on], zs = zc[c.os];
+    for (int kg = 0; kg < n_z; kg += NS) {
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const int k = kg + t;
+            if (k < n_z) {
+                const long long l = static_cast<long long>(k) * sm;
+                const T ce = ze, cw = zw, cn = zn, cs_ = zs;
+                if (k + 1 < n_z) {  // horizontal neighbours one level ahead
+                    ze = zc[l + sm + c.oe];
+                    zw = zc[l + sm + c.ow];
+                    zn = zc[l + sm + c.on];
+                    zs = zc[l + sm + c.os];
+                }
+                cp_wait<D - 1>();
+                const T* r0 = ring + t * 4 * NT;
+                T pv = r0[0], qv = r0[NT];
+                const T uv = r0[2 * NT];
+                const T zu = k + 1 < n_z ? r0[3 * NT] : z0;
+                if (k + D < n_z) issue(k + D, (t + D) & (NS - 1));
+                cp_commit();
+                __stcs(uc + l, A::add(uv, A::mul(alpha, pv)));
+                pv = A::add(A::mul(beta, pv), z0);
+                qv = A::mul(beta, qv);
+                __stcs(pc + l, pv);
+                const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw,
+                                              c.an, c.as, z0, zu, zd, ce, cw, cn, cs_);
+                qv = A::add(qv, A::mul(dP[k], dq));
+                sig = A::add(sig, A::mul(pv, qv));
+                __stcs(qc + l, qv);
+                zd = z0;
+                z0 = zu;
+            }
+        }
+    }
+    cp_wait<0>();
+    if (stage != nullptr) {  // fused reduction stage 1 (X = 8: one plane x 256 j, all valid)
+        __syncthreads();
+        ring[0] = sig;
+        __syncthreads();
+        if (threadIdx.y == 0)
+            cta_subtree_sums<T, NT>(prof + 4 * n_z, 1, stage, nleaves,
+                                    (static_cast<long long>(il) * m + blockIdx.x * NT) / NT);
+        return;
+    }
+    part[static_cast<long long>(il) * m + j] = sig;
+}
