@@ -130,15 +130,27 @@ __device__ __forceinline__ Col<T> load_col(const SlabView<T>& v, int il, int j) 
 template <typename T, int NT>
 __device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __restrict__ stage,
                                                  int nleaves, long long leaf) {
-    constexpr int B = NT / 8;  // sequential blocks per array
-    static_assert(B >= 1 && B <= 32 && (B & (B - 1)) == 0, "power-of-two block count");
+    constexpr int BT = NT / 8;                 // sequential blocks per array
+    constexpr int L = BT > 32 ? BT / 32 : 1;   // blocks per lane (perfect tree in registers)
+    constexpr int B = BT / L;                  // lanes per array
+    static_assert(BT >= 1 && (BT & (BT - 1)) == 0 && L * B == BT, "power-of-two block count");
     const int lane = threadIdx.x;
     const int a = lane / B, b = lane % B;
     T v = T(0);
     if (a < nv) {
-        const T* x = vals + a * NT + 8 * b;
+        T w[L];
 #pragma unroll
-        for (int l = 0; l < 8; ++l) v = add_rn(v, x[l]);
+        for (int i = 0; i < L; ++i) {
+            const T* x = vals + a * NT + 8 * (b * L + i);
+            w[i] = T(0);
+#pragma unroll
+            for (int l = 0; l < 8; ++l) w[i] = add_rn(w[i], x[l]);
+        }
+#pragma unroll
+        for (int st = 1; st < L; st <<= 1)
+#pragma unroll
+            for (int i = 0; i + st < L; i += 2 * st) w[i] = add_rn(w[i], w[i + st]);
+        v = w[0];
     }
 #pragma unroll
     for (int w = 1; w < B; w <<= 1) {
@@ -939,10 +951,15 @@ int launch_thomas_tm2_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
     return leaves;
 }
 
-inline int thomas_tm2_choice() {  // ACG_THOMAS_TM2=1 opts in (measured slower: 0.99 vs 0.80 ms)
+// Two columns per thread: default for fp32 (C4: K1 1.51 vs 2.09 ms, the fp32
+// sweep moves half the bytes per instruction), off for fp64 (C3: 0.99 vs
+// 0.80 ms). ACG_THOMAS_TM2=0/1 overrides.
+template <typename T>
+int thomas_tm2_choice() {
     static int c = [] {
         const char* e = std::getenv("ACG_THOMAS_TM2");
-        return e && std::string(e) == "1" ? 1 : 0;
+        if (e) return std::string(e) == "1" ? 1 : 0;
+        return sizeof(T) == 4 ? 1 : 0;
     }();
     return c;
 }
@@ -962,8 +979,8 @@ inline int thomas_tm_choice() {
         const char* e = std::getenv("ACG_THOMAS_TM");
         if (!e) return 1;
         const std::string s(e);
-        const char* names[] = {"0", "4,15,15", "4,15,15,1", "8,15,15", "2,15,15"};
-        for (int a = 0; a < 5; ++a)
+        const char* names[] = {"0", "4,15,15", "4,15,15,1", "8,15,15", "2,15,15", "q1", "q8", "q4"};
+        for (int a = 0; a < 8; ++a)
             if (s == names[a]) return a;
         return 1;
     }();
@@ -974,7 +991,7 @@ template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
                   const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
     const int tmc = thomas_tm_choice();
-    const int tm2 = thomas_tm2_choice();
+    const int tm2 = thomas_tm2_choice<T>();
     if (tm2 != 0 && tmc != 0 && v.tm_ok && phi_scratch == nullptr && !thomas_tma_enabled()) {
         int l = -1;
         l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Cfg<4, 15, 15>>(v, r, in, out, p2, pk, S,
@@ -993,6 +1010,9 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
             case 2: ACG_TM(ThomasTmCfg<4, 15, 15, 1>);
             case 3: ACG_TM(ThomasTmCfg<8, 15, 15>);
             case 4: ACG_TM(ThomasTmCfg<2, 15, 15>);
+            case 5: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 1>);
+            case 6: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 8>);
+            case 7: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 4>);
             default: ACG_TM(ThomasTmCfg<4, 15, 15>);
         }
 #undef ACG_TM
@@ -1081,7 +1101,12 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         if (e && std::string(e) == "tile") return 0;
         if (e && std::string(e) == "ring2") return 3;
         if (e && std::string(e) == "ring8") return 4;
-        return sizeof(T) == 4 ? 0 : 2;
+        if (e && std::string(e) == "pair") return 5;
+        return 5;  // pair kernel (falls back to the tile kernel for odd m)
+    }();
+    static const int pair_cfg = [] {  // ACG_SPMV_PAIR = 10*D + min CTAs per SM
+        const char* e = std::getenv("ACG_SPMV_PAIR");
+        return e ? std::atoi(e) : (sizeof(T) == 4 ? 23 : 22);
     }();
     static const int tile_d = [] {
         const char* e = std::getenv("ACG_SPMV_D");
@@ -1096,6 +1121,30 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             ensure_smem(k_fused_spmv<T, false>, smem);
             k_fused_spmv<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
         }
+    } else if (mode == 5 && v.m % 2 == 0) {
+        const int Dp = pair_cfg / 10;
+        leaves = fused_leaves(v, 2 * 32 * kStencilWarps, stage);
+        T* stg = leaves ? stage : nullptr;
+        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
+                                         static_cast<size_t>(Dp + 1) * 4 * 2 * 32 * kStencilWarps);
+        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps), v.m_loc);
+#define ACG_PR(F, DD, MB)                                                                         \
+    do {                                                                                          \
+        ensure_smem(k_fused_spmv_pair<T, F, DD, MB>, smem);                                       \
+        k_fused_spmv_pair<T, F, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
+    } while (0)
+        switch (fast ? -pair_cfg : pair_cfg) {
+            case 22: ACG_PR(false, 2, 2); break;
+            case 32: ACG_PR(false, 3, 2); break;
+            case 42: ACG_PR(false, 4, 2); break;
+            case 23: ACG_PR(false, 2, 3); break;
+            case 33: ACG_PR(false, 3, 3); break;
+            case 24: ACG_PR(false, 2, 4); break;
+            case -22: ACG_PR(true, 2, 2); break;
+            case -33: ACG_PR(true, 3, 3); break;
+            default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
+        }
+#undef ACG_PR
     } else if (mode == 4) {
         static const int Xenv = [] {
             const char* e = std::getenv("ACG_SPMV_X");
