@@ -1102,11 +1102,15 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         if (e && std::string(e) == "ring2") return 3;
         if (e && std::string(e) == "ring8") return 4;
         if (e && std::string(e) == "pair") return 5;
-        return 5;  // pair kernel (falls back to the tile kernel for odd m)
+        if (e && std::string(e) == "pair2") return 6;
+        // two-column kernels (the tile kernel for odd m): fp64 with every stencil
+        // input in the cp.async ring (C3 K2 1.18 ms), fp32 with the neighbour rows
+        // loaded a level ahead (C4 K2 2.59 ms); measured.
+        return sizeof(T) == 4 ? 5 : 6;
     }();
     static const int pair_cfg = [] {  // ACG_SPMV_PAIR = 10*D + min CTAs per SM
         const char* e = std::getenv("ACG_SPMV_PAIR");
-        return e ? std::atoi(e) : (sizeof(T) == 4 ? 23 : 22);
+        return e ? std::atoi(e) : (sizeof(T) == 4 ? 23 : 32);
     }();
     static const int tile_d = [] {
         const char* e = std::getenv("ACG_SPMV_D");
@@ -1142,6 +1146,31 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             case 24: ACG_PR(false, 2, 4); break;
             case -22: ACG_PR(true, 2, 2); break;
             case -33: ACG_PR(true, 3, 3); break;
+            default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
+        }
+#undef ACG_PR
+    } else if (mode == 6 && v.m % 2 == 0) {
+        const int Dp = pair_cfg / 10;
+        leaves = fused_leaves(v, 2 * 32 * kStencilWarps, stage);
+        T* stg = leaves ? stage : nullptr;
+        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
+                                         static_cast<size_t>(Dp + 1) * 7 * 2 * 32 * kStencilWarps);
+        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps), v.m_loc);
+#define ACG_PR(F, DD, MB)                                                                         \
+    do {                                                                                          \
+        ensure_smem(k_fused_spmv_pair2<T, F, DD, MB>, smem);                                      \
+        k_fused_spmv_pair2<T, F, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
+    } while (0)
+        switch (fast ? -pair_cfg : pair_cfg) {
+            case 22: ACG_PR(false, 2, 2); break;
+            case 32: ACG_PR(false, 3, 2); break;
+            case 23: ACG_PR(false, 2, 3); break;
+            case 13: ACG_PR(false, 1, 3); break;
+            case 41: ACG_PR(false, 4, 1); break;
+            case 51: ACG_PR(false, 5, 1); break;
+            case 31: ACG_PR(false, 3, 1); break;
+            case 33: ACG_PR(false, 3, 3); break;
+            case 43: ACG_PR(false, 4, 3); break;
             default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
         }
 #undef ACG_PR

@@ -487,3 +487,111 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     }
     *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};
 }
+
+template <typename T, bool Fast, int D, int MINB>
+__global__ void __launch_bounds__(32 * kStencilWarps, MINB)
+    k_fused_spmv_pair2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
+                      T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
+                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
+    using A = Ar<T, Fast>;
+    using P = Pair<T>;
+    constexpr int NT = 32 * kStencilWarps, NS = D + 1;
+    if (S->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);
+    __syncthreads();
+    const int il = blockIdx.y;
+    const int jr = blockIdx.x * 2 * NT + 2 * tid;
+    const bool valid = jr < m;  // m even: both columns exist
+    if (stage == nullptr && !valid) return;
+    const int j = valid ? jr : m - 2;
+    P* ring = reinterpret_cast<P*>(prof + 4 * n_z) + tid;  // [slot][7][NT] (6 pairs + 2 edge scalars)
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    const Col<T> ca = load_col(v, il, j);
+    const Col<T> cb = load_col(v, il, j + 1);
+    const T alpha = S->alpha, beta = S->beta;
+    const long long base = static_cast<long long>(il) * v.plane + j;
+    const T* zc = z + base;
+    T* uc = u + base;
+    T* pc = p + base;
+    T* qc = q + base;
+    const long long sm = m;
+    const long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+    auto issue = [&](int k, int s) {
+        const long long l = static_cast<long long>(k) * sm;
+        P* r0 = ring + s * 7 * NT;
+        cpa_pair<T>(r0, pc + l);
+        cpa_pair<T>(r0 + NT, qc + l);
+        cpa_pair<T>(r0 + 2 * NT, uc + l);
+        if (k + 1 < n_z) cpa_pair<T>(r0 + 3 * NT, zc + l + sm);
+        cpa_pair<T>(r0 + 4 * NT, zc + l + oe);
+        cpa_pair<T>(r0 + 5 * NT, zc + l + ow);
+        T* e = reinterpret_cast<T*>(r0 + 6 * NT);  // z(j-1), z(j+2) (own values on the edges)
+        cpa(e, zc + l + ca.os);
+        cpa(e + 1, zc + l + 1 + cb.on);
+    };
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        if (t < n_z) issue(t, t);
+        cp_commit();
+    }
+    P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
+    T siga = T(0), sigb = T(0);
+    int cs = 0, ps_ = D;
+    for (int k = 0; k < n_z; ++k) {
+        const long long l = static_cast<long long>(k) * sm;
+        cp_wait<D - 1>();
+        const P* r0 = ring + cs * 7 * NT;
+        P pv = r0[0], qv = r0[NT];
+        const P uv = r0[2 * NT];
+        const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
+        const P ce = r0[4 * NT], cw = r0[5 * NT];
+        const P ex = r0[6 * NT];
+        const T cs0 = ex.x, cn1 = ex.y;
+        if (k + D < n_z) issue(k + D, ps_);
+        cp_commit();
+        cs = cs + 1 == NS ? 0 : cs + 1;
+        ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
+        const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
+        pv.x = A::add(A::mul(beta, pv.x), z0.x);
+        pv.y = A::add(A::mul(beta, pv.y), z0.y);
+        qv.x = A::mul(beta, qv.x);
+        qv.y = A::mul(beta, qv.y);
+        // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
+        const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
+                                       ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
+        // column j+1: south = own .x, north = z(j+2) (own value on the edge)
+        const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
+                                       cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
+        qv.x = A::add(qv.x, A::mul(dP[k], dqa));
+        qv.y = A::add(qv.y, A::mul(dP[k], dqb));
+        siga = A::add(siga, A::mul(pv.x, qv.x));
+        sigb = A::add(sigb, A::mul(pv.y, qv.y));
+        if (valid) {
+            st_pair_cs(uc + l, un);
+            st_pair_cs(pc + l, pv);
+            st_pair_cs(qc + l, qv);
+        }
+        zd = z0;
+        z0 = zu;
+    }
+    cp_wait<0>();
+    if (stage != nullptr) {  // fused reduction stage 1: the CTA's 512 columns are a tree node
+        __syncthreads();
+        T* red = prof + 4 * n_z;
+        red[2 * tid] = siga;
+        red[2 * tid + 1] = sigb;
+        __syncthreads();
+        if (threadIdx.y == 0)
+            cta_subtree_sums<T, 2 * NT>(red, 1, stage, nleaves,
+                                        (static_cast<long long>(il) * m + blockIdx.x * 2 * NT) / (2 * NT));
+        return;
+    }
+    *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};
+}
