@@ -737,6 +737,51 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// Stage 2 with warp shuffles: NTH threads, C consecutive leaves each (perfect
+// tree in registers), then a shuffle tree per warp and a perfect tree over the
+// warps — the same perfect tree over nleaves = NTH * C leaves as k_tree2.
+template <typename T, int C>
+__global__ void __launch_bounds__(256)
+    k_tree2_shfl(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather,
+                 int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op) {
+    if (op != kOpStore && S->done) return;
+    __shared__ T wsum[3][8];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int width = nt < 32 ? nt : 32;
+    for (int a = 0; a < nv; ++a) {
+        T v[C];
+#pragma unroll
+        for (int l = 0; l < C; ++l) v[l] = stage[a * static_cast<long long>(nleaves) + tid * C + l];
+#pragma unroll
+        for (int w = 1; w < C; w <<= 1)
+#pragma unroll
+            for (int l = 0; l + w < C; l += 2 * w) v[l] = add_rn(v[l], v[l + w]);
+        T x = v[0];
+        for (int w = 1; w < width; w <<= 1) {
+            const T o = __shfl_down_sync(0xffffffffu >> (32 - width), x, w, width);
+            if ((lane & (2 * w - 1)) == 0) x = add_rn(x, o);
+        }
+        if (lane == 0) wsum[a][warp] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int nw = (nt + 31) / 32;
+        T sums[4] = {T(0), T(0), T(0), T(0)};
+        for (int a = 0; a < nv; ++a) {
+            T w8[8];
+            for (int w = 0; w < nw; ++w) w8[w] = wsum[a][w];
+            for (int st = 1; st < nw; st <<= 1)
+                for (int w = 0; w + st < nw; w += 2 * st) w8[w] = add_rn(w8[w], w8[w + st]);
+            gather[slab * 4 + a] = w8[0];
+        }
+        if (finish) {
+            for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
+            run_op(S, op, sums);
+        }
+    }
+}
+
 template <typename T>
 __global__ void k_finish(const T* __restrict__ gather, int nv, int nslabs, int exact,
                          Scalars<T>* __restrict__ S, int op) {
@@ -979,8 +1024,8 @@ inline int thomas_tm_choice() {
         const char* e = std::getenv("ACG_THOMAS_TM");
         if (!e) return 1;
         const std::string s(e);
-        const char* names[] = {"0", "4,15,15", "4,15,15,1", "8,15,15", "2,15,15", "q1", "q8", "q4"};
-        for (int a = 0; a < 8; ++a)
+        const char* names[] = {"0", "4,15,15", "4,15,15,1", "8,15,15", "2,15,15", "q1", "q8", "q4", "q8b"};
+        for (int a = 0; a < 9; ++a)
             if (s == names[a]) return a;
         return 1;
     }();
@@ -1013,6 +1058,7 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
             case 5: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 1>);
             case 6: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 8>);
             case 7: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 4>);
+            case 8: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 8>);
             default: ACG_TM(ThomasTmCfg<4, 15, 15>);
         }
 #undef ACG_TM
@@ -1381,8 +1427,29 @@ template <typename T>
 void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
                         bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
                         cudaStream_t st) {
-    const int nt = plan.blocks < 1024 ? plan.blocks : 1024;
-    k_tree2<T><<<1, nt, 0, st>>>(plan.blocks, stage, nv, gather, slab, finish ? 1 : 0, nslabs,
+    const int nl = plan.blocks;  // power of two
+    static const bool legacy = [] {
+        const char* e = std::getenv("ACG_TREE2");
+        return e && std::string(e) == "legacy";
+    }();
+    if (!legacy && nl <= 256 * 64) {
+        const int c = nl > 256 ? nl / 256 : 1;
+        const int nt = nl / c;
+        const int f = finish ? 1 : 0, ex = exact_tree ? 1 : 0;
+        switch (c) {
+            case 1: k_tree2_shfl<T, 1><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            case 2: k_tree2_shfl<T, 2><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            case 4: k_tree2_shfl<T, 4><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            case 8: k_tree2_shfl<T, 8><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            case 16: k_tree2_shfl<T, 16><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            case 32: k_tree2_shfl<T, 32><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            default: k_tree2_shfl<T, 64><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+        }
+        post_launch("tree2");
+        return;
+    }
+    const int nt = nl < 1024 ? nl : 1024;
+    k_tree2<T><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, finish ? 1 : 0, nslabs,
                                  exact_tree ? 1 : 0, S, op);
     post_launch("tree2");
 }
