@@ -145,6 +145,14 @@ acg_status acg_field_create(acg_field** out, const acg_context* ctx);
 acg_status acg_field_destroy(acg_field* f);
 acg_status acg_field_upload(acg_field* f, const void* host, acg_layout layout, acg_host_scope scope);
 acg_status acg_field_download(const acg_field* f, void* host, acg_layout layout, acg_host_scope scope);
+/* Device-resident counterparts of upload/download: `dev` is a device buffer
+ * (CUDA pointer, e.g. a torch/CuPy tensor's data) in the same host layout
+ * convention; the relayout runs on the context's stream and the call returns
+ * without synchronising (order later host work with acg_synchronize). */
+acg_status acg_field_upload_device(acg_field* f, const void* dev, acg_layout layout,
+                                   acg_host_scope scope);
+acg_status acg_field_download_device(const acg_field* f, void* dev, acg_layout layout,
+                                     acg_host_scope scope);
 acg_status acg_field_fill(acg_field* f, double value);
 /* fill_random, field.hpp:180-196 (splitmix64, canonical (i,j,k) draw order) */
 acg_status acg_field_fill_random(acg_field* f, uint64_t seed);

@@ -47,6 +47,34 @@ except ImportError as exc:  # pragma: no cover - the product must not run withou
 
 LIBRARY_PATH = _os.path.join(_HERE, "libacg_cuda.so")
 
+from . import _anisocg as _ext  # noqa: E402
+from . import capi as _capi  # noqa: E402
+from . import device as _device  # noqa: E402
+
+
+def solve(ctx, f, *args, **kw):
+    """solve(ctx, f, u0=None, epsilon=1e-5, tau=1e-20, maxiter=500, variant="interleaved",
+    backend="matrix-free", workers=1, *, layout="vertical") -> (u, SolveResult).
+    Host (numpy) arrays: the reference binding (bindings.cpp:204-237). CUDA arrays
+    (torch, CuPy): device-resident, no PCIe transfer (device.solve)."""
+    if _capi.is_cuda_array(f):
+        return _device.solve(ctx, f, *args, **kw)
+    return _ext.solve(ctx, f, *args, **kw)
+
+
+def apply(ctx, x, *args, **kw):
+    """y = A x; numpy in/out (reference binding) or CUDA arrays in/out (device.apply)."""
+    if _capi.is_cuda_array(x):
+        return _device.apply(ctx, x, *args, **kw)
+    return _ext.apply(ctx, x, *args, **kw)
+
+
+def precondition(ctx, y, *args, **kw):
+    """x = M^-1 y; numpy in/out (reference binding) or CUDA arrays in/out (device.precondition)."""
+    if _capi.is_cuda_array(y):
+        return _device.precondition(ctx, y, *args, **kw)
+    return _ext.precondition(ctx, y, *args, **kw)
+
 __all__ = [
     "KernelTimings", "OperatorContext", "OperatorContextF32", "PanelGeometry", "SolveResult",
     "VerticalGrid", "VerticalProfile", "anisotropy", "apply", "assemble_csr", "axpy",

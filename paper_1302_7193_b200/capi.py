@@ -98,6 +98,8 @@ def lib():
         "acg_field_destroy": (ip, [vp]),
         "acg_field_upload": (ip, [vp, vp, ip, ip]),
         "acg_field_download": (ip, [vp, vp, ip, ip]),
+        "acg_field_upload_device": (ip, [vp, vp, ip, ip]),
+        "acg_field_download_device": (ip, [vp, vp, ip, ip]),
         "acg_field_fill": (ip, [vp, C.c_double]),
         "acg_field_fill_random": (ip, [vp, C.c_uint64]),
         "acg_field_copy": (ip, [vp, vp]),
@@ -208,6 +210,21 @@ class Context:
         self._children = weakref.WeakSet()  # fields/solvers released before the context
 
     @classmethod
+    def borrow(cls, handle, owner=None):
+        """View of an existing acg_context (e.g. an anisocg.OperatorContext's);
+        does not destroy it. `owner` is kept alive for the view's lifetime."""
+        self = cls.__new__(cls)
+        self.h = C.c_void_p(handle)
+        inf = ContextInfo()
+        check(lib().acg_context_info_get(self.h, C.byref(inf)))
+        self.m, self.n_z, self.dtype = inf.m, inf.n_z, inf.dtype
+        self.np_dtype = np.float32 if inf.dtype == F32 else np.float64
+        self._children = weakref.WeakSet()
+        self._owner = owner
+        self._borrowed = True
+        return self
+
+    @classmethod
     def from_setup(cls, profile, panel, **kw):
         """From (a', b', c', d) and (area, east, north, diag) arrays."""
         return cls(*profile, *panel, **kw)
@@ -231,7 +248,8 @@ class Context:
         if self.h:
             for child in list(self._children):
                 child.close()
-            lib().acg_context_destroy(self.h)
+            if not getattr(self, "_borrowed", False):
+                lib().acg_context_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -239,6 +257,31 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def is_cuda_array(a):
+    """True for device arrays exposing __cuda_array_interface__ (torch, CuPy)."""
+    return hasattr(a, "__cuda_array_interface__")
+
+
+def cuda_array_ptr(a, dtype, shape):
+    """Device pointer of a C-contiguous CUDA array of `dtype` and `shape`
+    (raises ValueError otherwise, like the reference's nonconformant-field check)."""
+    ai = a.__cuda_array_interface__
+    if np.dtype(ai["typestr"]) != np.dtype(dtype):
+        raise ValueError(f"device array dtype {np.dtype(ai['typestr'])} != context dtype {np.dtype(dtype)}")
+    if tuple(ai["shape"]) != tuple(shape):
+        raise ValueError(f"device array shape {tuple(ai['shape'])} != expected {tuple(shape)}")
+    st = ai.get("strides")
+    if st is not None:
+        item = np.dtype(dtype).itemsize
+        want, acc = [], item
+        for d in reversed(shape):
+            want.append(acc)
+            acc *= d
+        if tuple(st) != tuple(reversed(want)):
+            raise ValueError("device array must be C-contiguous")
+    return int(ai["data"][0])
 
 
 class Field:
@@ -250,16 +293,33 @@ class Field:
         self.h, self.ctx = h, ctx
         ctx._children.add(self)
 
+    def _shape(self, layout, scope):
+        m, n_z = self.ctx.m, self.ctx.n_z
+        inf = self.ctx.info() if scope == HOST_LOCAL else None
+        ml = inf["i_end"] - inf["i_begin"] if inf else m
+        return (ml, m, n_z) if layout == VERTICAL else (m, n_z, ml)
+
     def upload(self, a, layout=VERTICAL, scope=HOST_FULL):
+        """From a host array, or zero-PCIe from a CUDA array (torch/CuPy:
+        anything with __cuda_array_interface__) on the context's device."""
+        if is_cuda_array(a):
+            ptr = cuda_array_ptr(a, self.ctx.np_dtype, self._shape(layout, scope))
+            check(lib().acg_field_upload_device(self.h, C.c_void_p(ptr), layout, scope))
+            self.ctx.sync()  # the source buffer belongs to another stream's owner
+            return self
         a = np.ascontiguousarray(a, dtype=self.ctx.np_dtype)
         check(lib().acg_field_upload(self.h, _vptr(a), layout, scope))
         return self
 
     def download(self, layout=VERTICAL, out=None, scope=HOST_FULL):
-        m, n_z = self.ctx.m, self.ctx.n_z
+        """To a host array, or (out = a CUDA array) device to device."""
+        if out is not None and is_cuda_array(out):
+            ptr = cuda_array_ptr(out, self.ctx.np_dtype, self._shape(layout, scope))
+            check(lib().acg_field_download_device(self.h, C.c_void_p(ptr), layout, scope))
+            self.ctx.sync()
+            return out
         if out is None:
-            shape = (m, m, n_z) if layout == VERTICAL else (m, n_z, m)
-            out = np.empty(shape, dtype=self.ctx.np_dtype)
+            out = np.empty(self._shape(layout, scope), dtype=self.ctx.np_dtype)
         check(lib().acg_field_download(self.h, _vptr(out), layout, scope))
         return out
 

@@ -643,6 +643,55 @@ void download_t(const acg_field* f, void* host, acg_layout layout, acg_host_scop
     CK(cudaStreamSynchronize(c->stream));
 }
 
+// Device-resident counterparts (the Python edge hands over torch/CuPy device
+// buffers): the relayout kernel reads / writes the caller's buffer directly,
+// no staging and no PCIe traffic.
+template <typename T>
+void upload_dev_t(acg_field* f, const void* dev, acg_layout layout, acg_host_scope scope) {
+    const acg_context* c = f->ctx;
+    const int m = c->m, n_z = c->n_z;
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        T* dst = static_cast<T*>(f->data(si));
+        const T* src = static_cast<const T*>(dev);
+        if (layout == ACG_LAYOUT_VERTICAL) {
+            if (scope == ACG_HOST_FULL) src += static_cast<size_t>(s.i0) * m * n_z;
+            launch_transpose<T>(src, dst, n_z, m, s.m_loc, n_z, static_cast<long long>(m) * n_z, m,
+                                s.plane, c->stream);
+        } else if (scope == ACG_HOST_FULL) {  // src[(j*n_z + k)*m + i0 + il]
+            launch_transpose<T>(src + s.i0, dst, s.m_loc, m, n_z, static_cast<long long>(n_z) * m,
+                                m, s.plane, m, c->stream);
+        } else {
+            launch_transpose<T>(src, dst, s.m_loc, m, n_z, static_cast<long long>(n_z) * s.m_loc,
+                                s.m_loc, s.plane, m, c->stream);
+        }
+        CK(cudaPeekAtLastError());
+    }
+}
+
+template <typename T>
+void download_dev_t(const acg_field* f, void* dev, acg_layout layout, acg_host_scope scope) {
+    const acg_context* c = f->ctx;
+    const int m = c->m, n_z = c->n_z;
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        const T* src = static_cast<const T*>(f->data(si));
+        T* dst = static_cast<T*>(dev);
+        if (layout == ACG_LAYOUT_VERTICAL) {
+            if (scope == ACG_HOST_FULL) dst += static_cast<size_t>(s.i0) * m * n_z;
+            launch_transpose<T>(src, dst, m, n_z, s.m_loc, m, s.plane, n_z,
+                                static_cast<long long>(m) * n_z, c->stream);
+        } else if (scope == ACG_HOST_FULL) {  // dst[(j*n_z + k)*m + i0 + il]
+            launch_transpose<T>(src, dst + s.i0, m, s.m_loc, n_z, s.plane, m,
+                                static_cast<long long>(n_z) * m, m, c->stream);
+        } else {
+            launch_transpose<T>(src, dst, m, s.m_loc, n_z, s.plane, m,
+                                static_cast<long long>(n_z) * s.m_loc, s.m_loc, c->stream);
+        }
+        CK(cudaPeekAtLastError());
+    }
+}
+
 // ---------------------------------------------------------------- halos
 // Ghost plane -1 of slab s <- plane m_loc-1 of slab s-1; ghost plane m_loc of
 // slab s <- plane 0 of slab s+1. Device copies between local slabs, NCCL
@@ -868,6 +917,26 @@ acg_status acg_field_download(const acg_field* f, void* host, acg_layout layout,
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
         ACG_TDISPATCH(c, download_t<T>(f, host, layout, scope));
+    });
+}
+
+acg_status acg_field_upload_device(acg_field* f, const void* dev, acg_layout layout,
+                                   acg_host_scope scope) {
+    return guarded([&] {
+        if (!f || !dev) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = f->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, upload_dev_t<T>(f, dev, layout, scope));
+    });
+}
+
+acg_status acg_field_download_device(const acg_field* f, void* dev, acg_layout layout,
+                                     acg_host_scope scope) {
+    return guarded([&] {
+        if (!f || !dev) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = f->ctx;
+        DeviceGuard g(c->device);
+        ACG_TDISPATCH(c, download_dev_t<T>(f, dev, layout, scope));
     });
 }
 

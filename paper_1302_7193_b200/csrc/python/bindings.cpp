@@ -9,6 +9,7 @@
 #include <pybind11/stl.h>
 
 #include <array>
+#include <cstdint>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -153,6 +154,9 @@ void bind_context(py::module_& mod, const char* name) {
              py::arg("math") = "exact", py::arg("device") = 0)
         .def_property_readonly("m", &OperatorContext<T>::m)
         .def_property_readonly("n_z", &OperatorContext<T>::n_z)
+        .def_property_readonly("_handle", [](const OperatorContext<T>& c) {
+            return reinterpret_cast<std::uintptr_t>(c.device());
+        })
         .def_property_readonly("info", [](const OperatorContext<T>& c) {
             acg_context_info i{};
             detail::check(acg_context_info_get(c.device(), &i));

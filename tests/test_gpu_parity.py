@@ -345,3 +345,53 @@ def test_fused_reduction_stage_bit_exact(acg, m, n_z):
     ug, rg, uo, ro = _solve_both(acg, o, ctx, f, 0, epsilon=1e-300, maxiter=6)
     assert _same_result(rg, ro)
     assert np.array_equal(ug, uo)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("layout", ["vertical", "horizontal"])
+def test_device_resident_edge(acg, dtype, layout):
+    """torch CUDA tensors in and out of solve/apply/precondition (device.py): no
+    PCIe copy of the field, same bits as the host path and the CPU reference."""
+    import torch
+    prob = Problem(24, 16)
+    o = Oracle(prob)
+    ctx = ctx_for(acg, prob, dtype)
+    lay_i = 0 if layout == "vertical" else 1
+    f = o.random_field(42, dtype, lay_i)
+    ft = torch.from_numpy(f).cuda()
+    u_h, r_h = acg.solve(ctx, f, epsilon=1e-6, maxiter=200, layout=layout)
+    u_t, r_t = acg.solve(ctx, ft, epsilon=1e-6, maxiter=200, layout=layout)
+    assert isinstance(u_t, torch.Tensor) and u_t.is_cuda and u_t.dtype == ft.dtype
+    assert np.array_equal(u_t.cpu().numpy(), u_h)
+    assert r_t.iterations == r_h.iterations and r_t.converged == r_h.converged
+    assert np.array_equal(r_t.residual_history, r_h.residual_history)
+    assert np.array_equal(acg.apply(ctx, ft, layout=layout).cpu().numpy(), o.apply(f, lay_i))
+    assert np.array_equal(acg.precondition(ctx, ft, layout=layout).cpu().numpy(),
+                          o.precondition(f, lay_i))
+    with pytest.raises(ValueError):
+        acg.solve(ctx, ft[:-1].contiguous(), layout=layout)
+    with pytest.raises(ValueError):
+        acg.apply(ctx, ft.to(torch.float16), layout=layout)
+
+
+def test_capi_device_buffers_slabs(acg):
+    """acg_field_upload_device / download_device over a multi-slab context and
+    the HOST_LOCAL scope of one slab's i-range."""
+    import torch
+    from paper_1302_7193_b200 import capi
+    prob = Problem(32, 12)
+    o = Oracle(prob)
+    ctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag, slabs=4)
+    x = o.random_field(9)
+    xt = torch.from_numpy(x).cuda()
+    fld = ctx.field().upload(xt)
+    assert np.array_equal(fld.download(), x)
+    back = torch.empty_like(xt)
+    fld.download(out=back)
+    assert torch.equal(back, xt)
+    xh = torch.from_numpy(np.ascontiguousarray(x.transpose(1, 2, 0))).cuda()
+    f2 = ctx.field().upload(xh, capi.HORIZONTAL)
+    assert np.array_equal(f2.download(), x)
+    back_h = torch.empty_like(xh)
+    f2.download(capi.HORIZONTAL, out=back_h)
+    assert torch.equal(back_h, xh)
