@@ -18,7 +18,8 @@ CXXFLAGS:= -O2 -std=c++20 -fPIC -Wall -ffp-contract=off -Iinclude -I$(CUDA)/incl
 
 LIB     := $(PKG)/libacg_cuda.so
 PYMOD   := $(PKG)/_anisocg$(EXT)
-HOSTSRC := $(CSRC)/host/grid.cpp $(CSRC)/host/profile.cpp $(CSRC)/host/shim.cpp
+HOSTSRC := $(CSRC)/host/grid.cpp $(CSRC)/host/profile.cpp $(CSRC)/host/shim.cpp \
+           $(CSRC)/host/cost_model.cpp $(CSRC)/host/io.cpp
 HDRS    := include/acg.h $(wildcard include/anisocg/*.hpp) $(CSRC)/acg_internal.h
 
 .PHONY: all lib py oracle clean

@@ -9,6 +9,7 @@
 #include <pybind11/stl.h>
 
 #include <array>
+#include <sstream>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -17,6 +18,7 @@
 #include "acg.h"
 #include "anisocg/field.hpp"
 #include "anisocg/grid.hpp"
+#include "anisocg/io.hpp"
 #include "anisocg/operator.hpp"
 #include "anisocg/profile.hpp"
 #include "anisocg/solver.hpp"
@@ -425,6 +427,53 @@ PYBIND11_MODULE(_anisocg, mod) {
         },
         py::arg("m"), py::arg("n_z"), py::arg("seed") = 42, py::kw_only(),
         py::arg("dtype") = "float64", "The deterministic benchmark right-hand side (GPU generated)");
+    // report and wire formats (io.hpp); the text is returned for the caller to write
+    mod.def(
+        "residual_csv",
+        [](py::object r) {
+            SolveResult res;
+            py::object h = py::hasattr(r, "residual_history") ? r.attr("residual_history") : r;
+            const Arr<double> a = h.cast<Arr<double>>();
+            res.residual_history.assign(a.data(), a.data() + a.size());
+            std::ostringstream os;
+            io::write_residual_csv(os, res);
+            return os.str();
+        },
+        py::arg("result"), "io::write_residual_csv as a string (a SolveResult or a history array)");
+    mod.def(
+        "cost_model_csv",
+        [] {
+            std::ostringstream os;
+            io::write_cost_model_csv(os);
+            return os.str();
+        },
+        "io::write_cost_model_csv as a string");
+    mod.def(
+        "geometry_csv",
+        [](const PanelGeometry& g) {
+            std::ostringstream os;
+            io::write_geometry_csv(os, g);
+            return os.str();
+        },
+        py::arg("geometry"), "io::write_geometry_csv as a string");
+    mod.def(
+        "dump_field",
+        [](py::array a, const std::string& layout) {
+            const Layout L = parse_layout(layout);
+            const bool vert = L == Layout::VerticalContiguous;
+            if (a.ndim() != 3) throw std::invalid_argument("expected a 3D field array");
+            const int m = static_cast<int>(a.shape(0));
+            const int n_z = static_cast<int>(vert ? a.shape(2) : a.shape(1));
+            std::ostringstream os;
+            if (py::isinstance<py::array_t<float>>(a)) {
+                io::dump_field(os, to_field<float>(a.cast<Arr<float>>(), m, n_z, L));
+            } else {
+                io::dump_field(os, to_field<double>(a.cast<Arr<double>>(), m, n_z, L));
+            }
+            return py::bytes(os.str());
+        },
+        py::arg("field"), py::kw_only(), py::arg("layout") = "vertical",
+        "io::dump_field: text header + raw little-endian values (bytes)");
     mod.def("kernel_launch_count", &acg_kernel_launch_count,
             "Device kernels launched by this process through libacg_cuda.so");
 }
