@@ -160,6 +160,50 @@ __device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __res
     if (a < nv && b == 0) stage[a * static_cast<long long>(nleaves) + leaf] = v;
 }
 
+template <typename T>
+__device__ void run_op(Scalars<T>* S, int op, const T* sums);
+
+// Device view of Finish<T> passed to the sweeps (op < 0: off).
+template <typename T>
+struct FinishDev {
+    Scalars<T>* S;
+    int* counter;
+    int op;
+};
+
+// Last-CTA finish (single slab): after every CTA has written its node sums to
+// stage[a * nleaves + leaf], the CTA that arrives last reduces the nleaves
+// (a power of two) of each array with the perfect tree (k_tree2's order) in
+// shared memory `buf` (>= nleaves values) and runs the scalar program.
+template <typename T>
+__device__ void cta_finish(const FinishDev<T>& fin, const T* stage, int nleaves, int nv, T* buf,
+                           int tid, int nthreads) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(fin.counter, 1) == static_cast<int>(gridDim.x * gridDim.y) - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    T sums[4] = {T(0), T(0), T(0), T(0)};
+    for (int a = 0; a < nv; ++a) {
+        for (int l = tid; l < nleaves; l += nthreads)
+            buf[l] = __ldcg(stage + static_cast<long long>(a) * nleaves + l);
+        __syncthreads();
+        for (int st = 1; st < nleaves; st <<= 1) {
+            for (int i = tid * 2 * st; i < nleaves; i += nthreads * 2 * st)
+                buf[i] = add_rn(buf[i], buf[i + st]);
+            __syncthreads();
+        }
+        sums[a] = buf[0];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        run_op(fin.S, fin.op, sums);
+        *fin.counter = 0;
+    }
+}
+
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
 #include "acg_thomas_tm.cuh"
@@ -895,20 +939,33 @@ int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
 // beyond that would only wait inside tcgen05.alloc).
 template <typename T, bool Fast, bool Fused, class C>
 int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
-                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
+                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st,
+                         Finish<T>* fin = nullptr) {
     const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
     const dim3 block(32, C::W);
     constexpr int PW = C::W / C::X;  // i-planes per CTA
     const dim3 grid((v.m + 32 * C::X - 1) / (32 * C::X), (v.m_loc + PW - 1) / PW);
     size_t smem = thomas_tm_smem_bytes<T, C>(v.n_z);
-    const size_t max_ctas = 512u / tcols;
+    static const size_t occ_cap = [] {  // ACG_TM_OCC=n caps resident CTAs per SM (experiments)
+        const char* e = std::getenv("ACG_TM_OCC");
+        return static_cast<size_t>(e ? std::atoi(e) : 0);
+    }();
+    size_t max_ctas = 512u / tcols;
+    if (occ_cap > 0 && occ_cap < max_ctas) max_ctas = occ_cap;
     const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
     if (smem < floor_bytes) smem = floor_bytes;
     // fused stage 1: CTA = one aligned node (128 consecutive columns) of the tree
     const int leaves = fused_leaves(v, C::X == 4 ? C::NT : 0, Fused ? stage : nullptr);
+    FinishDev<T> fd{nullptr, nullptr, -1};
+    // the finish tree needs `leaves` values of the (then free) shared memory after the profile
+    if (fin && leaves > 0 &&
+        static_cast<size_t>(leaves) + kTmProf * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
+        fd = {fin->S, fin->counter, fin->op};
+        fin->used = true;
+    }
     ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
     k_thomas_tm<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, tcols,
-                                                             leaves ? stage : nullptr, leaves);
+                                                             leaves ? stage : nullptr, leaves, fd);
     return leaves;
 }
 
@@ -1034,7 +1091,8 @@ inline int thomas_tm_choice() {
 
 template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
-                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
+                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st,
+                  Finish<T>* fin = nullptr) {
     const int tmc = thomas_tm_choice();
     const int tm2 = thomas_tm2_choice<T>();
     if (tm2 != 0 && tmc != 0 && v.tm_ok && phi_scratch == nullptr && !thomas_tma_enabled()) {
@@ -1050,7 +1108,7 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
         if (l >= 0) return l;
     }
     if (tmc != 0 && v.tm_ok && phi_scratch == nullptr && thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
-#define ACG_TM(...) return launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, stage, st)
+#define ACG_TM(...) return launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, stage, st, fin)
         switch (tmc) {
             case 2: ACG_TM(ThomasTmCfg<4, 15, 15, 1>);
             case 3: ACG_TM(ThomasTmCfg<8, 15, 15>);
@@ -1109,12 +1167,13 @@ bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st) {
 
 template <typename T>
 int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st) {
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st,
+                      Finish<T>* fin) {
     const int leaves =
         fast ? launch_thomas<T, true, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
-                                            stage, st)
+                                            stage, st, fin)
              : launch_thomas<T, false, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
-                                             stage, st);
+                                             stage, st, fin);
     post_launch("fused_prec");
     return leaves;
 }
@@ -1133,7 +1192,7 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
 
 template <typename T>
 int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                      const Scalars<T>* S, T* stage, cudaStream_t st) {
+                      const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin) {
     int leaves = 0;
     const dim3 block(32, kStencilWarps);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
@@ -1145,8 +1204,6 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         if (e && std::string(e) == "plain") return 1;
         if (e && std::string(e) == "ring") return 2;
         if (e && std::string(e) == "tile") return 0;
-        if (e && std::string(e) == "ring2") return 3;
-        if (e && std::string(e) == "ring8") return 4;
         if (e && std::string(e) == "pair") return 5;
         if (e && std::string(e) == "pair2") return 6;
         // two-column kernels (the tile kernel for odd m): fp64 with every stencil
@@ -1202,10 +1259,16 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                          static_cast<size_t>(Dp + 1) * 7 * 2 * 32 * kStencilWarps);
         const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps), v.m_loc);
+        FinishDev<T> fd{nullptr, nullptr, -1};
+        if (fin && leaves > 0 &&
+            static_cast<size_t>(leaves) + 4 * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
+            fd = {fin->S, fin->counter, fin->op};
+            fin->used = true;
+        }
 #define ACG_PR(F, DD, MB)                                                                         \
     do {                                                                                          \
         ensure_smem(k_fused_spmv_pair2<T, F, DD, MB>, smem);                                      \
-        k_fused_spmv_pair2<T, F, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
+        k_fused_spmv_pair2<T, F, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves, fd); \
     } while (0)
         switch (fast ? -pair_cfg : pair_cfg) {
             case 22: ACG_PR(false, 2, 2); break;
@@ -1220,58 +1283,6 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
         }
 #undef ACG_PR
-    } else if (mode == 4) {
-        static const int Xenv = [] {
-            const char* e = std::getenv("ACG_SPMV_X");
-            return e ? std::atoi(e) : 0;
-        }();
-        static const int Denv = [] {
-            const char* e = std::getenv("ACG_SPMV_D");
-            return e ? std::atoi(e) : 6;
-        }();
-        const int X = Xenv ? Xenv
-                           : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
-        if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
-        T* stg = leaves ? stage : nullptr;
-        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) + 8 * 4 * 32 * kStencilWarps);
-#define ACG_R8(F, XX, DD)                                                                         \
-    do {                                                                                          \
-        const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
-                      (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
-        ensure_smem(k_fused_spmv_ring8<T, F, XX, DD>, smem);                                      \
-        k_fused_spmv_ring8<T, F, XX, DD><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
-    } while (0)
-        if (fast) {
-            if (X == 8) ACG_R8(true, 8, 6); else if (X == 4) ACG_R8(true, 4, 6); else if (X == 2) ACG_R8(true, 2, 6); else ACG_R8(true, 1, 6);
-        } else if (X == 8) {
-            if (Denv == 7) ACG_R8(false, 8, 7); else if (Denv == 5) ACG_R8(false, 8, 5); else if (Denv == 4) ACG_R8(false, 8, 4); else ACG_R8(false, 8, 6);
-        } else {
-            if (X == 4) ACG_R8(false, 4, 6); else if (X == 2) ACG_R8(false, 2, 6); else ACG_R8(false, 1, 6);
-        }
-#undef ACG_R8
-    } else if (mode == 3) {
-        static const int Xenv = [] {
-            const char* e = std::getenv("ACG_SPMV_X");
-            return e ? std::atoi(e) : 0;
-        }();
-        const int X = Xenv ? Xenv
-                           : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
-        if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
-        T* stg = leaves ? stage : nullptr;
-        const size_t smem = spmv_ring2_smem_bytes<T>(v.n_z);
-#define ACG_R2(F, XX)                                                                             \
-    do {                                                                                          \
-        const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
-                      (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
-        ensure_smem(k_fused_spmv_ring2<T, F, XX, 3>, smem);                                       \
-        k_fused_spmv_ring2<T, F, XX, 3><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
-    } while (0)
-        if (fast) {
-            if (X == 2) ACG_R2(true, 2); else if (X == 4) ACG_R2(true, 4); else if (X == 8) ACG_R2(true, 8); else ACG_R2(true, 1);
-        } else {
-            if (X == 2) ACG_R2(false, 2); else if (X == 4) ACG_R2(false, 4); else if (X == 8) ACG_R2(false, 8); else ACG_R2(false, 1);
-        }
-#undef ACG_R2
     } else if (mode == 2) {
         // ring depth: D levels (or 10*D + min CTAs/SM); measured best at C3:
         // D = 2 with 4 CTAs (32 warps) per SM, 1.28 vs 1.33 ms for D = 6 with 3
@@ -1474,11 +1485,11 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
 #define ACG_INSTANTIATE(T)                                                                      \
     template bool validate_thomas_tm<T>(const SlabView<T>&, cudaStream_t);                      \
     template int launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,       \
-                                      Scalars<T>*, T*, T*, cudaStream_t);                       \
+                                      Scalars<T>*, T*, T*, cudaStream_t, Finish<T>*);           \
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
                                          const Scalars<T>*, T*, cudaStream_t);                  \
     template int launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,       \
-                                      const Scalars<T>*, T*, cudaStream_t);                     \
+                                      const Scalars<T>*, T*, cudaStream_t, Finish<T>*);         \
     template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \
                                   cudaStream_t);                                                \
     template void launch_residual_partials<T>(const SlabView<T>&, bool, const T*, const T*, T*, \

@@ -136,6 +136,7 @@ struct Slab {
     void* tmp = nullptr;  // Scalars<T> for API calls
     TreePlan plan{};
     bool tm_ok = false;   // TMEM Thomas sweep usable (validate_thomas_tm)
+    int* fin_counter = nullptr;  // last-CTA finish counter of the fused sweeps (zero at rest)
 };
 
 size_t dsize(acg_dtype t) { return t == ACG_F32 ? sizeof(float) : sizeof(double); }
@@ -271,7 +272,8 @@ void build_slab_tables(const acg_context* c, Slab& s, const acg_operator_desc* d
 }
 
 void free_slab(Slab& s) {
-    void* ps[] = {s.prof, s.col, s.part[0], s.part[1], s.part[2], s.stage, s.phi, s.staging, s.tmp};
+    void* ps[] = {s.prof, s.col, s.part[0], s.part[1], s.part[2], s.stage, s.phi, s.staging, s.tmp,
+                  s.fin_counter};
     for (void* p : ps)
         if (p) cudaFree(p);
     s = Slab{};
@@ -448,6 +450,8 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
             if (s.plan.blocks > 16384)
                 fail(ACG_ERR_INVALID_ARGUMENT, "slab of %lld columns exceeds the reduction plan",
                      ncol);
+            CK(cudaMalloc(&s.fin_counter, sizeof(int)));
+            CK(cudaMemset(s.fin_counter, 0, sizeof(int)));
             // stage: k_tree1 block sums, or up to 16384 node sums written by a sweep
             CK(cudaMalloc(&s.stage, 3 * static_cast<size_t>(std::max(s.plan.blocks, 16384)) * c->s));
             if (thomas_smem_per_block(static_cast<int>(c->s), d->n_z, false) > 200 * 1024)
@@ -1371,6 +1375,16 @@ void iterate_interleaved(acg_solver* s) {
     auto S = sv<T>(s);
     std::vector<int>& leaves = s->leaves;
     leaves.resize(c->slabs.size());
+    // Single slab, opt-in (ACG_CTA_FINISH=1): the sweep's last CTA finishes the
+    // reduction instead of a k_tree2 launch. Measured slower at C3 (2.027 vs
+    // 2.004 ms/iter): the one-CTA tail tree over 8192 leaves costs more than
+    // the launch it saves.
+    static const bool cta_finish = [] {
+        const char* e = std::getenv("ACG_CTA_FINISH");
+        return e && std::string(e) == "1";
+    }();
+    const bool single = c->nslabs_total == 1 && cta_finish;
+    Finish<T> fin1{S[0], c->slabs[0].fin_counter, kOpIlPrec, false};
     s->timer.begin(kFusedPrec);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& sl = c->slabs[si];
@@ -1379,23 +1393,25 @@ void iterate_interleaved(acg_solver* s) {
             view<T>(c, si), c->fast(), static_cast<T*>(s->r->data(si)),
             static_cast<T*>(s->z->data(si)), static_cast<const T*>(s->q->data(si)),
             static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), S[si],
-            static_cast<T*>(sl.phi), static_cast<T*>(sl.stage), c->stream);
+            static_cast<T*>(sl.phi), static_cast<T*>(sl.stage), c->stream,
+            single ? &fin1 : nullptr);
         s->ktimer.end(kFusedPrec);
     }
-    reduce<T>(c, 2, kOpIlPrec, S, nullptr, true, &leaves);
+    if (!fin1.used) reduce<T>(c, 2, kOpIlPrec, S, nullptr, true, &leaves);
     s->timer.end(kFusedPrec);
     s->timer.begin(kFusedSpmv);
     halo(c, s->z);
+    Finish<T> fin2{S[0], c->slabs[0].fin_counter, kOpIlSpmv, false};
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         s->ktimer.begin(kFusedSpmv);
         leaves[si] = launch_fused_spmv<T>(
             view<T>(c, si), c->fast(), static_cast<T*>(s->u->data(si)),
             static_cast<T*>(s->p->data(si)), static_cast<T*>(s->q->data(si)),
             static_cast<const T*>(s->z->data(si)), static_cast<T*>(c->slabs[si].part[0]), S[si],
-            static_cast<T*>(c->slabs[si].stage), c->stream);
+            static_cast<T*>(c->slabs[si].stage), c->stream, single ? &fin2 : nullptr);
         s->ktimer.end(kFusedSpmv);
     }
-    reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true, &leaves);
+    if (!fin2.used) reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true, &leaves);
     s->timer.end(kFusedSpmv);
 }
 

@@ -150,219 +150,7 @@ __global__ void __launch_bounds__(32 * W)
     if (valid) part[static_cast<long long>(il) * m + j] = sig;
 }
 
-// K2, all stencil inputs through the per-thread cp.async ring (fp64 default).
-// ncu on k_fused_spmv_ring: the i+-1 neighbour loads, even issued a level
-// ahead, still held ~1/4 of the warp samples (those rows belong to other
-// CTAs and often come from DRAM). Here every level's p, q, u, z(k+1), the two
-// i-neighbour rows z(i+-1, k) and, for the warp's edge lanes, the j-neighbour
-// beyond the warp are copied D levels ahead; the j+-1 neighbours inside the
-// warp come from the own z row by shuffles. CTA = one i-plane x 32*X j.
-template <typename T, bool Fast, int X, int D>
-__global__ void __launch_bounds__(32 * kStencilWarps)
-    k_fused_spmv_ring2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
-                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                       const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
-    using A = Ar<T, Fast>;
-    constexpr int NT = 32 * kStencilWarps, NS = 4, NA = 7;
-    static_assert(D >= 1 && D < NS, "prefetch depth below the ring size");
-    if (S->done) return;  // block-uniform
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* prof = reinterpret_cast<T*>(smem_raw);
-    const int n_z = v.n_z, m = v.m;
-    const int lane = threadIdx.x;
-    const int tid = threadIdx.y * 32 + lane;
-    load_profile(prof, v.prof, 4 * n_z, tid, NT);
-    const int jw = (blockIdx.x * X + threadIdx.y % X) * 32;  // first column of this warp
-    const int jr = jw + lane;
-    const int il = blockIdx.y * (kStencilWarps / X) + threadIdx.y / X;
-    const bool valid = jr < m && il < v.m_loc;
-    const int j = jr < m ? jr : m - 1;
-    const int ilc = il < v.m_loc ? il : v.m_loc - 1;
-    T* ring = prof + 4 * n_z + tid;  // [slot][NA][NT]
-    const T* sP = prof + kProfS * n_z;
-    const T* bP = prof + kProfB * n_z;
-    const T* cP = prof + kProfC * n_z;
-    const T* dP = prof + kProfD * n_z;
-    const Col<T> c = load_col(v, ilc, j);
-    const long long base = static_cast<long long>(ilc) * v.plane + j;
-    const T* zc = z + base;
-    T* uc = u + base;
-    T* pc = p + base;
-    T* qc = q + base;
-    // edge lanes fetch the j-neighbour outside the warp (clamped into the row)
-    const bool edge = lane == 0 || lane == 31;
-    const int je = lane == 0 ? (jw > 0 ? jw - 1 : 0) : (jw + 32 < m ? jw + 32 : m - 1);
-    const T* zedge = z + static_cast<long long>(ilc) * v.plane + je;
-    const long long sm = m;
-    auto issue = [&](int kk, int slot) {
-        T* r0 = ring + slot * NA * NT;
-        const long long l = kk * sm;
-        cpa(r0 + 0 * NT, pc + l);
-        cpa(r0 + 1 * NT, qc + l);
-        cpa(r0 + 2 * NT, uc + l);
-        if (kk + 1 < n_z) cpa(r0 + 3 * NT, zc + l + sm);
-        cpa(r0 + 4 * NT, zc + l + c.oe);
-        cpa(r0 + 5 * NT, zc + l + c.ow);
-        if (edge) cpa(r0 + 6 * NT, zedge + l);
-    };
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        if (t < n_z) issue(t, t);
-        cp_commit();
-    }
-    __syncthreads();  // profile
-    const T alpha = S->alpha, beta = S->beta;
-    T z0 = zc[0], zd = z0, sig = T(0);
-    for (int kg = 0; kg < n_z; kg += NS) {
-#pragma unroll
-        for (int t = 0; t < NS; ++t) {
-            const int k = kg + t;
-            if (k < n_z) {  // block-uniform
-                cp_wait<D - 1>();
-                const T* r0 = ring + t * NA * NT;
-                T pv = r0[0], qv = r0[NT];
-                const T uv = r0[2 * NT];
-                const T zu = k + 1 < n_z ? r0[3 * NT] : z0;
-                const T ze = r0[4 * NT], zw = r0[5 * NT];
-                const T zx = edge ? r0[6 * NT] : T(0);
-                if (k + D < n_z) issue(k + D, (t + D) & (NS - 1));
-                cp_commit();
-                T zn = __shfl_down_sync(0xffffffffu, z0, 1);
-                T zs = __shfl_up_sync(0xffffffffu, z0, 1);
-                if (lane == 31) zn = zx;
-                if (lane == 0) zs = zx;
-                if (c.on == 0) zn = z0;  // panel edge: own value, coefficient 0 (operator.hpp:85-92)
-                if (c.os == 0) zs = z0;
-                const long long l = static_cast<long long>(k) * sm;
-                const T un = A::add(uv, A::mul(alpha, pv));
-                pv = A::add(A::mul(beta, pv), z0);
-                qv = A::mul(beta, qv);
-                const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw,
-                                              c.an, c.as, z0, zu, zd, ze, zw, zn, zs);
-                qv = A::add(qv, A::mul(dP[k], dq));
-                sig = A::add(sig, A::mul(pv, qv));
-                if (valid) {
-                    __stcs(uc + l, un);
-                    __stcs(pc + l, pv);
-                    __stcs(qc + l, qv);
-                }
-                zd = z0;
-                z0 = zu;
-            }
-        }
-    }
-    cp_wait<0>();
-    if (stage != nullptr) {  // fused reduction stage 1 (X = 8: one plane x 256 j, all valid)
-        __syncthreads();
-        ring[0] = sig;
-        __syncthreads();
-        if (threadIdx.y == 0)
-            cta_subtree_sums<T, NT>(prof + 4 * n_z, 1, stage, nleaves,
-                                    (static_cast<long long>(il) * m + blockIdx.x * NT) / NT);
-        return;
-    }
-    if (valid) part[static_cast<long long>(il) * m + jr] = sig;
-}
 
-template <typename T>
-__host__ __device__ constexpr size_t spmv_ring2_smem_bytes(int n_z) {
-    return sizeof(T) * (4 * static_cast<size_t>(n_z) + 4 * 7 * static_cast<size_t>(32 * kStencilWarps));
-}
-
-// K2, k_fused_spmv_ring with an 8-slot ring unrolled by 8 (slot offsets are
-// immediates, no modular slot counters) and prefetch depth D <= 7.
-template <typename T, bool Fast, int X, int D>
-__global__ void __launch_bounds__(32 * kStencilWarps)
-    k_fused_spmv_ring8(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
-                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                       const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
-    using A = Ar<T, Fast>;
-    constexpr int NT = 32 * kStencilWarps, NS = 8;
-    static_assert(D >= 1 && D < NS, "prefetch depth below the ring size");
-    if (S->done) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* prof = reinterpret_cast<T*>(smem_raw);
-    const int n_z = v.n_z, m = v.m;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    load_profile(prof, v.prof, 4 * n_z, tid, NT);
-    __syncthreads();
-    const int j = (blockIdx.x * X + threadIdx.y % X) * 32 + threadIdx.x;
-    const int il = blockIdx.y * (kStencilWarps / X) + threadIdx.y / X;
-    if (stage == nullptr && (j >= m || il >= v.m_loc)) return;
-    T* ring = prof + 4 * n_z + tid;  // [slot][4][NT]
-    const T* sP = prof + kProfS * n_z;
-    const T* bP = prof + kProfB * n_z;
-    const T* cP = prof + kProfC * n_z;
-    const T* dP = prof + kProfD * n_z;
-    const Col<T> c = load_col(v, il, j);
-    const T alpha = S->alpha, beta = S->beta;
-    const long long base = static_cast<long long>(il) * v.plane + j;
-    const T* zc = z + base;
-    T* uc = u + base;
-    T* pc = p + base;
-    T* qc = q + base;
-    const long long sm = m;
-    auto issue = [&](int k, int s) {
-        const long long l = static_cast<long long>(k) * sm;
-        T* r0 = ring + s * 4 * NT;
-        cpa(r0, pc + l);
-        cpa(r0 + NT, qc + l);
-        cpa(r0 + 2 * NT, uc + l);
-        if (k + 1 < n_z) cpa(r0 + 3 * NT, zc + l + sm);
-    };
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        if (t < n_z) issue(t, t);
-        cp_commit();
-    }
-    T z0 = zc[0], zd = z0, sig = T(0);
-    T ze = zc[c.oe], zw = zc[c.ow], zn = zc[c.on], zs = zc[c.os];
-    for (int kg = 0; kg < n_z; kg += NS) {
-#pragma unroll
-        for (int t = 0; t < NS; ++t) {
-            const int k = kg + t;
-            if (k < n_z) {
-                const long long l = static_cast<long long>(k) * sm;
-                const T ce = ze, cw = zw, cn = zn, cs_ = zs;
-                if (k + 1 < n_z) {  // horizontal neighbours one level ahead
-                    ze = zc[l + sm + c.oe];
-                    zw = zc[l + sm + c.ow];
-                    zn = zc[l + sm + c.on];
-                    zs = zc[l + sm + c.os];
-                }
-                cp_wait<D - 1>();
-                const T* r0 = ring + t * 4 * NT;
-                T pv = r0[0], qv = r0[NT];
-                const T uv = r0[2 * NT];
-                const T zu = k + 1 < n_z ? r0[3 * NT] : z0;
-                if (k + D < n_z) issue(k + D, (t + D) & (NS - 1));
-                cp_commit();
-                __stcs(uc + l, A::add(uv, A::mul(alpha, pv)));
-                pv = A::add(A::mul(beta, pv), z0);
-                qv = A::mul(beta, qv);
-                __stcs(pc + l, pv);
-                const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw,
-                                              c.an, c.as, z0, zu, zd, ce, cw, cn, cs_);
-                qv = A::add(qv, A::mul(dP[k], dq));
-                sig = A::add(sig, A::mul(pv, qv));
-                __stcs(qc + l, qv);
-                zd = z0;
-                z0 = zu;
-            }
-        }
-    }
-    cp_wait<0>();
-    if (stage != nullptr) {  // fused reduction stage 1 (X = 8: one plane x 256 j, all valid)
-        __syncthreads();
-        ring[0] = sig;
-        __syncthreads();
-        if (threadIdx.y == 0)
-            cta_subtree_sums<T, NT>(prof + 4 * n_z, 1, stage, nleaves,
-                                    (static_cast<long long>(il) * m + blockIdx.x * NT) / NT);
-        return;
-    }
-    part[static_cast<long long>(il) * m + j] = sig;
-}
 
 __device__ __forceinline__ void st_pair_cs(double* a, const Pair<double>& v) {
     __stcs(reinterpret_cast<double2*>(a), make_double2(v.x, v.y));
@@ -492,7 +280,8 @@ template <typename T, bool Fast, int D, int MINB>
 __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     k_fused_spmv_pair2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
+                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves,
+                      const FinishDev<T> fin) {
     using A = Ar<T, Fast>;
     using P = Pair<T>;
     constexpr int NT = 32 * kStencilWarps, NS = D + 1;
@@ -591,6 +380,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         if (threadIdx.y == 0)
             cta_subtree_sums<T, 2 * NT>(red, 1, stage, nleaves,
                                         (static_cast<long long>(il) * m + blockIdx.x * 2 * NT) / (2 * NT));
+        if (fin.op >= 0) cta_finish(fin, stage, nleaves, 1, red, tid, NT);
         return;
     }
     *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};
