@@ -196,7 +196,8 @@ def workload(cfg, args, n):
                         f"interleaved matrix-free PCG (paper Alg. 1-3)",
             "m": cfg["m"], "n_z": cfg["n_z"], "omega2": OMEGA2, "lambda2": cfg["lambda2"],
             "h_atmos": H, "seed": 42, "math": args.math, "variant": args.variant,
-            "parallelism": f"{n} i-slab(s), one per GPU" if n > 1 else "1 GPU",
+            "parallelism": (f"{n} i-slabs, one per GPU, {args.transport} transport" if n > 1
+                            else "1 GPU"),
             "l2": "no flush: every field (N*s bytes) exceeds the 126 MB L2"}
 
 
@@ -206,15 +207,27 @@ def run_gpu(args, cfg):
     from paper_1302_7193_b200 import capi
 
     rank, world, local = dist_env()
-    dev = local
+    # ACG_SAME_GPU=1 puts every rank on GPU 0 (functional runs of the multi-rank path
+    # on a one-GPU box; the torch process group is then gloo, the transport must be ipc)
+    same_gpu = os.environ.get("ACG_SAME_GPU") == "1"
+    dev = 0 if same_gpu else local
     torch.cuda.set_device(dev)
     comm = None
+    pg_dev = "cpu" if same_gpu else "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        obj = [capi.Comm.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        comm = capi.Comm(rank, world, obj[0], dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if args.transport == "nccl":
+            obj = [capi.Comm.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            comm = capi.Comm(rank, world, obj[0], dev)
+        else:  # peer memory (CUDA IPC mailboxes over NVLink P2P), no NCCL on the data path
+            obj = [os.urandom(16) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            comm = capi.Comm.ipc(rank, world, obj[0], dev)
     dtype = capi.F32 if cfg["dtype"] == "f32" else capi.F64
     s = 4 if dtype == capi.F32 else 8
     math_mode = capi.FAST if args.math == "fast" else capi.EXACT
@@ -259,7 +272,7 @@ def run_gpu(args, cfg):
     ms_max = ms
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=pg_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     it_s = args.steps / (ms_max * 1e-3)
@@ -326,7 +339,7 @@ def run_gpu(args, cfg):
         split = {"upload_s": t1 - t0, "solve_s": t2 - t1, "download_s": time.perf_counter() - t2}
         if world > 1:
             import torch.distributed as dist
-            t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+            t = torch.tensor([wall], device=pg_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
         nbytes = ml * m * n_z * s
@@ -386,6 +399,9 @@ def main():
     ap.add_argument("--math", default="exact", choices=["exact", "fast"])
     ap.add_argument("--variant", default="interleaved", choices=["interleaved", "standard"])
     ap.add_argument("--slabs", type=int, default=1, help="virtual slabs on one GPU (N=1)")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1 halo/reduction transport: peer-memory mailboxes (CUDA IPC over "
+                         "NVLink) or NCCL send/recv + all-gather")
     ap.add_argument("--cpu-iters", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -99,6 +99,7 @@ def lib():
         "acg_field_upload": (ip, [vp, vp, ip, ip]),
         "acg_field_download": (ip, [vp, vp, ip, ip]),
         "acg_field_upload_device": (ip, [vp, vp, ip, ip]),
+        "acg_comm_create_ipc": (ip, [pp, ip, ip, vp, ip]),
         "acg_field_download_device": (ip, [vp, vp, ip, ip]),
         "acg_field_fill": (ip, [vp, C.c_double]),
         "acg_field_fill_random": (ip, [vp, C.c_uint64]),
@@ -177,6 +178,17 @@ class Comm:
         buf = C.create_string_buffer(unique_id, 128)
         check(lib().acg_comm_create(C.byref(h), rank, nranks, buf, device))
         self.h, self.rank, self.nranks = h, rank, nranks
+
+    @classmethod
+    def ipc(cls, rank, nranks, unique_id: bytes, device):
+        """Peer-memory communicator (acg_comm_create_ipc): ranks of one node,
+        CUDA IPC mailboxes, no NCCL. unique_id: same bytes on every rank."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id)[:128].ljust(128, b"\0"), 128)
+        check(lib().acg_comm_create_ipc(C.byref(h), rank, nranks, buf, device))
+        self.h, self.rank, self.nranks = h, rank, nranks
+        return self
 
     @staticmethod
     def unique_id() -> bytes:

@@ -170,6 +170,22 @@ template <typename T>
 void launch_finish(const T* gather, int nv, int nslabs, bool exact_tree, Scalars<T>* S, int op,
                    cudaStream_t st);
 
+// Peer-memory (CUDA IPC) transport between the ranks of one node. Flags are
+// 64-bit sequence numbers in the owner's mailbox, written by peers with
+// system-scope release stores after their data landed, polled with acquire
+// loads (a poll that does not complete within ~20 s traps instead of hanging).
+//  signal: flags[i] = seq for the non-null entries of flags[0..n)
+//  wait:   until flags[i] >= seq for the entries of `need` (bit i)
+void launch_ipc_signal(unsigned long long* const* flags, int n, unsigned long long seq,
+                       cudaStream_t st);
+void launch_ipc_wait(const unsigned long long* flags, int n, unsigned long long need,
+                     unsigned long long seq, cudaStream_t st);
+// every rank's 4 slab sums: src (4 T) -> dst[q] + rank*4 for q < n, then
+// flag[q] (in rank q's mailbox) = seq; dst and flag are device arrays of n pointers
+template <typename T>
+void launch_ipc_put_sums(const T* src, T* const* dst, unsigned long long* const* flag, int n,
+                         int rank, unsigned long long seq, cudaStream_t st);
+
 // relayout between the reference's host layouts and plane-major (K7):
 // out[x*osx + y + b*osb] = in[x + y*isy + b*isb]  for x<nx, y<ny, b<nb
 template <typename T>

@@ -835,6 +835,52 @@ __global__ void k_finish(const T* __restrict__ gather, int nv, int nslabs, int e
     run_op(S, op, sums);
 }
 
+// ------------------------------------------------------- peer-memory transport
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct FlagPtrs {
+    unsigned long long* f[8];
+};
+
+__global__ void k_ipc_signal(FlagPtrs fp, int n, unsigned long long seq) {
+    __threadfence_system();  // the data this flag publishes (copies earlier on the stream)
+    for (int i = 0; i < n; ++i)
+        if (fp.f[i]) st_release_sys(fp.f[i], seq);
+}
+
+__global__ void k_ipc_wait(const unsigned long long* flags, int n, unsigned long long need,
+                           unsigned long long seq) {
+    const long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+        if (!((need >> i) & 1ull)) continue;
+        while (ld_acquire_sys(flags + i) < seq) {
+            if (clock64() - t0 > (40ll << 30)) __trap();  // a peer never arrived: fail, do not hang
+            __nanosleep(64);
+        }
+    }
+    __threadfence_system();
+}
+
+template <typename T>
+__global__ void k_ipc_put_sums(const T* __restrict__ src, T* const* __restrict__ dst,
+                               unsigned long long* const* __restrict__ flag, int n, int rank,
+                               unsigned long long seq) {
+    const int q = threadIdx.x;
+    if (q < n) {
+        T* d = dst[q] + rank * 4;
+        for (int a = 0; a < 4; ++a) d[a] = src[a];
+        __threadfence_system();
+        st_release_sys(flag[q] + rank, seq);
+    }
+}
+
 // --------------------------------------------------------- launch helpers
 inline void post_launch(const char* what) {
     ++g_launches;
@@ -1472,6 +1518,27 @@ void launch_finish(const T* gather, int nv, int nslabs, bool exact_tree, Scalars
     post_launch("finish");
 }
 
+void launch_ipc_signal(unsigned long long* const* flags, int n, unsigned long long seq,
+                       cudaStream_t st) {
+    FlagPtrs fp{};
+    for (int i = 0; i < n && i < 8; ++i) fp.f[i] = flags[i];
+    k_ipc_signal<<<1, 1, 0, st>>>(fp, n < 8 ? n : 8, seq);
+    post_launch("ipc_signal");
+}
+
+void launch_ipc_wait(const unsigned long long* flags, int n, unsigned long long need,
+                     unsigned long long seq, cudaStream_t st) {
+    k_ipc_wait<<<1, 1, 0, st>>>(flags, n, need, seq);
+    post_launch("ipc_wait");
+}
+
+template <typename T>
+void launch_ipc_put_sums(const T* src, T* const* dst, unsigned long long* const* flag, int n,
+                         int rank, unsigned long long seq, cudaStream_t st) {
+    k_ipc_put_sums<T><<<1, 64, 0, st>>>(src, dst, flag, n, rank, seq);
+    post_launch("ipc_put_sums");
+}
+
 template <typename T>
 void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy, long long isb,
                       long long osx, long long osb, cudaStream_t st) {
@@ -1507,6 +1574,8 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
     template void launch_tree_stage2<T>(const TreePlan&, const T*, int, T*, int, bool, int,     \
                                         bool, Scalars<T>*, int, cudaStream_t);                  \
     template void launch_finish<T>(const T*, int, int, bool, Scalars<T>*, int, cudaStream_t);   \
+    template void launch_ipc_put_sums<T>(const T*, T* const*, unsigned long long* const*, int,   \
+                                         int, unsigned long long, cudaStream_t);                 \
     template void launch_transpose<T>(const T*, T*, int, int, int, long long, long long,        \
                                       long long, long long, cudaStream_t);
 

@@ -7,6 +7,8 @@
 // the loop never waits on the host.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <unistd.h>
 #include <nccl.h>  // types only; NCCL itself is dlopen'ed on first use
 
 #include <algorithm>
@@ -15,6 +17,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -118,7 +121,124 @@ void nccl_check(ncclResult_t r, const char* what) {
 struct acg_comm {
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1, device = 0;
+    int kind = 0;           // 0: NCCL, 1: peer memory (CUDA IPC, one node)
+    unsigned char uid[16];  // IPC: rendezvous namespace
+    int contexts = 0;       // IPC: contexts created on this communicator (rendezvous key)
 };
+
+namespace {
+
+// Peer-memory transport state of one context (acg_comm_create_ipc). Every rank
+// owns a mailbox: flags (halo from below / above, one reduction flag per rank),
+// two parities of the two ghost planes, two parities of all ranks' slab sums.
+// Peers write into it through CUDA IPC mappings (NVLink P2P between GPUs).
+struct IpcState {
+    int rank = 0, p = 1;
+    char* mbox = nullptr;
+    size_t bytes = 0, plane_bytes = 0, off_ghost = 0, off_gather = 0;
+    std::vector<char*> peer;  // mailbox of every rank (own = mbox)
+    void* dptr = nullptr;     // device: T* sums_dst[2][p], u64* red_flag[p]
+    unsigned long long halo_seq = 0, red_seq = 0;
+    std::string file;
+    unsigned long long* flags(int q) const { return reinterpret_cast<unsigned long long*>(peer[q]); }
+    char* ghost(int q, int parity, int side) const {  // side 0: from below (-1), 1: from above
+        return peer[q] + off_ghost + (static_cast<size_t>(parity) * 2 + side) * plane_bytes;
+    }
+    char* gather(int q, int parity, size_t s) const {
+        return peer[q] + off_gather + static_cast<size_t>(parity) * p * 4 * s;
+    }
+};
+
+std::string hex16(const unsigned char* b) {
+    static const char* d = "0123456789abcdef";
+    std::string o;
+    for (int i = 0; i < 16; ++i) {
+        o += d[b[i] >> 4];
+        o += d[b[i] & 15];
+    }
+    return o;
+}
+
+struct IpcRecord {
+    unsigned magic;
+    int rank;
+    unsigned long long bytes;
+    cudaIpcMemHandle_t handle;
+};
+
+// Allocate this rank's mailbox, publish its IPC handle under /dev/shm and map
+// every peer's (files keyed by the communicator's id and context ordinal).
+std::unique_ptr<IpcState> ipc_attach(acg_comm* comm, long long plane, size_t s) {
+    auto st = std::make_unique<IpcState>();
+    st->rank = comm->rank;
+    st->p = comm->nranks;
+    const int p = st->p;
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    st->plane_bytes = up(static_cast<size_t>(plane) * s);
+    st->off_ghost = up(8 * static_cast<size_t>(2 + p));
+    st->off_gather = st->off_ghost + 4 * st->plane_bytes;
+    st->bytes = st->off_gather + up(2 * static_cast<size_t>(p) * 4 * s);
+    CK(cudaMalloc(&st->mbox, st->bytes));
+    CK(cudaMemset(st->mbox, 0, st->bytes));
+    CK(cudaDeviceSynchronize());
+    IpcRecord rec{0xAC61BC01u, st->rank, st->bytes, {}};
+    CK(cudaIpcGetMemHandle(&rec.handle, st->mbox));
+    const std::string stem = "/dev/shm/acg-" + hex16(comm->uid) + "-" +
+                             std::to_string(comm->contexts++) + "-";
+    st->file = stem + std::to_string(st->rank);
+    {
+        const std::string tmp = st->file + ".tmp";
+        FILE* fh = std::fopen(tmp.c_str(), "wb");
+        if (!fh || std::fwrite(&rec, sizeof rec, 1, fh) != 1)
+            fail(ACG_ERR_INTERNAL, "IPC rendezvous: cannot write %s", tmp.c_str());
+        std::fclose(fh);
+        if (std::rename(tmp.c_str(), st->file.c_str()) != 0)
+            fail(ACG_ERR_INTERNAL, "IPC rendezvous: cannot publish %s", st->file.c_str());
+    }
+    st->peer.assign(p, nullptr);
+    st->peer[st->rank] = st->mbox;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int q = 0; q < p; ++q) {
+        if (q == st->rank) continue;
+        const std::string f = stem + std::to_string(q);
+        IpcRecord r{};
+        for (;;) {
+            FILE* fh = std::fopen(f.c_str(), "rb");
+            if (fh) {
+                const bool ok = std::fread(&r, sizeof r, 1, fh) == 1;
+                std::fclose(fh);
+                if (ok && r.magic == rec.magic && r.rank == q) break;
+            }
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+                fail(ACG_ERR_INTERNAL, "IPC rendezvous: rank %d never published %s", q, f.c_str());
+            std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        }
+        if (r.bytes != st->bytes)
+            fail(ACG_ERR_INVALID_ARGUMENT, "IPC rendezvous: rank %d has a different context", q);
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, r.handle, cudaIpcMemLazyEnablePeerAccess));
+        st->peer[q] = static_cast<char*>(ptr);
+    }
+    // device pointer tables for k_ipc_put_sums
+    std::vector<void*> tab(3 * static_cast<size_t>(p));
+    for (int par = 0; par < 2; ++par)
+        for (int q = 0; q < p; ++q) tab[par * p + q] = st->gather(q, par, s);
+    for (int q = 0; q < p; ++q) tab[2 * p + q] = st->flags(q) + 2;
+    CK(cudaMalloc(&st->dptr, tab.size() * sizeof(void*)));
+    CK(cudaMemcpy(st->dptr, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    return st;
+}
+
+void ipc_detach(IpcState* st) {
+    if (!st) return;
+    for (int q = 0; q < st->p; ++q)
+        if (q != st->rank && st->peer[q]) cudaIpcCloseMemHandle(st->peer[q]);
+    if (st->dptr) cudaFree(st->dptr);
+    if (st->mbox) cudaFree(st->mbox);
+    if (!st->file.empty()) unlink(st->file.c_str());
+}
+
+}  // namespace
 
 // ================================================================== context
 namespace {
@@ -171,6 +291,7 @@ struct acg_context {
     void* gather_send = nullptr;  // 4 T (NCCL)
     std::vector<acg_field*> pool; // reusable scratch fields (host entry points)
     acg_solver* cached = nullptr; // solver state reused by acg_solve / acg_solve_host
+    std::unique_ptr<IpcState> ipc; // peer-memory transport (acg_comm_create_ipc)
     size_t s = 8;
     bool fast() const { return math == ACG_MATH_FAST; }
 };
@@ -375,6 +496,22 @@ acg_status acg_comm_create(acg_comm** out, int rank, int nranks, const void* id1
     });
 }
 
+acg_status acg_comm_create_ipc(acg_comm** out, int rank, int nranks, const void* id128,
+                               int device) {
+    return guarded([&] {
+        if (!out || !id128) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            fail(ACG_ERR_INVALID_ARGUMENT, "bad rank %d of %d", rank, nranks);
+        auto c = std::make_unique<acg_comm>();
+        c->rank = rank;
+        c->nranks = nranks;
+        c->device = device;
+        c->kind = 1;
+        std::memcpy(c->uid, id128, sizeof c->uid);
+        *out = c.release();
+    });
+}
+
 acg_status acg_comm_destroy(acg_comm* c) {
     return guarded([&] {
         if (!c) return;
@@ -460,6 +597,8 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
         CK(cudaMalloc(&c->gather, static_cast<size_t>(p) * 4 * c->s));
         CK(cudaMemset(c->gather, 0, static_cast<size_t>(p) * 4 * c->s));
         CK(cudaMalloc(&c->gather_send, 4 * c->s));
+        if (c->comm && c->comm->kind == 1 && p > 1)
+            c->ipc = ipc_attach(c->comm, c->slabs[0].plane, c->s);
         *out = c.release();
     });
 }
@@ -490,6 +629,7 @@ acg_status acg_context_destroy(acg_context* c) {
         for (Slab& s : c->slabs) free_slab(s);
         if (c->gather) cudaFree(c->gather);
         if (c->gather_send) cudaFree(c->gather_send);
+        ipc_detach(c->ipc.get());
         if (c->stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -718,6 +858,33 @@ void halo(const acg_context* c, const acg_field* f) {
         }
         return;
     }
+    if (c->ipc) {  // peer memory: write the boundary planes into the neighbours' mailboxes
+        IpcState& ip = *c->ipc;
+        const int r = ip.rank, p = ip.p, m_loc = c->slabs[0].m_loc;
+        const unsigned long long seq = ++ip.halo_seq;
+        const int par = static_cast<int>(seq & 1);
+        unsigned long long* fl[2] = {nullptr, nullptr};
+        if (r > 0) {  // my plane 0 is the ghost "from above" of rank r-1
+            CK(cudaMemcpyAsync(ip.ghost(r - 1, par, 1), plane_ptr(0, 0), pb, cudaMemcpyDeviceToDevice,
+                               c->stream));
+            fl[0] = ip.flags(r - 1) + 1;
+        }
+        if (r + 1 < p) {  // my last plane is the ghost "from below" of rank r+1
+            CK(cudaMemcpyAsync(ip.ghost(r + 1, par, 0), plane_ptr(0, m_loc - 1), pb,
+                               cudaMemcpyDeviceToDevice, c->stream));
+            fl[1] = ip.flags(r + 1) + 0;
+        }
+        launch_ipc_signal(fl, 2, seq, c->stream);
+        launch_ipc_wait(ip.flags(r), 2, (r > 0 ? 1ull : 0ull) | (r + 1 < p ? 2ull : 0ull), seq,
+                        c->stream);
+        if (r > 0)
+            CK(cudaMemcpyAsync(plane_ptr(0, -1), ip.ghost(r, par, 0), pb, cudaMemcpyDeviceToDevice,
+                               c->stream));
+        if (r + 1 < p)
+            CK(cudaMemcpyAsync(plane_ptr(0, m_loc), ip.ghost(r, par, 1), pb,
+                               cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
     NcclApi& api = nccl();
     const int r = c->rank, p = c->nslabs_total;
     const Slab& s = c->slabs[0];
@@ -765,7 +932,19 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
                               c->nslabs_total, c->exact_tree, S[si], op, c->stream);
     }
     if (single) return;
-    if (c->comm) {
+    if (c->ipc) {  // peer memory: every rank's slab sums into every mailbox
+        IpcState& ip = *c->ipc;
+        const unsigned long long seq = ++ip.red_seq;
+        const int par = static_cast<int>(seq & 1);
+        T* const* dst = static_cast<T* const*>(ip.dptr) + static_cast<size_t>(par) * ip.p;
+        unsigned long long* const* fl =
+            reinterpret_cast<unsigned long long* const*>(static_cast<void* const*>(ip.dptr) + 2 * ip.p);
+        launch_ipc_put_sums<T>(static_cast<const T*>(c->gather_send), dst, fl, ip.p, ip.rank, seq,
+                               c->stream);
+        launch_ipc_wait(ip.flags(ip.rank) + 2, ip.p, ip.p >= 64 ? ~0ull : ((1ull << ip.p) - 1), seq,
+                        c->stream);
+        gather = reinterpret_cast<T*>(ip.gather(ip.rank, par, c->s));
+    } else if (c->comm) {
         const ncclDataType_t dt = c->dtype == ACG_F32 ? ncclFloat32 : ncclFloat64;
         nccl_check(nccl().allGather(c->gather_send, c->gather, 4, dt, c->comm->comm, c->stream),
                    "ncclAllGather");
