@@ -1,0 +1,54 @@
+"""Bit-exact parity at the BASELINE benchmark sizes (a few PCG iterations).
+
+The GPU solve of config 3 (fp64 1024^2 x 128, the headline workload), config 4
+(fp32 2048^2 x 128, lambda^2 = 100) and config 5 (fp64 4096^2 x 64, 8.6 GB per
+field; skipped on hosts with < 128 GB RAM) is compared with the reference's
+own code compiled from source (oracle/_ref, OpenMP on all host cores) on the
+same inputs: identical residual/kappa/alpha/beta histories and solution, bit
+for bit. Plus size-independent properties of the full-size fields.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Problem, Reference, ref_available
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {
+    "c3": dict(m=1024, n_z=128, dtype=np.float64, lambda2=3.32e-2, iters=3),
+    "c4": dict(m=2048, n_z=128, dtype=np.float32, lambda2=1.0e2, iters=2),
+    "c5": dict(m=4096, n_z=64, dtype=np.float64, lambda2=3.32e-2, iters=2),
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(CONFIGS))
+def test_full_size_bit_exact(acg, cfg):
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    c = CONFIGS[cfg]
+    if cfg == "c5":
+        with open("/proc/meminfo") as fh:
+            kb = int(fh.readline().split()[1])
+        if kb < 128 * 1024 * 1024:
+            pytest.skip("config 5 needs ~100 GB of host RAM for the reference")
+    prob = Problem(c["m"], c["n_z"], True, 6.71e-4, c["lambda2"], 1e-2)
+    g = acg.vertical_grid(prob.n_z, prob.h)
+    pro = acg.vertical_profile(g, prob.omega2, prob.lambda2)
+    cls = acg.OperatorContextF32 if c["dtype"] == np.float32 else acg.OperatorContext
+    ctx = cls(pro, acg.cubed_sphere_panel(prob.m))
+    dt = "float32" if c["dtype"] == np.float32 else "float64"
+    f = acg.random_field(prob.m, prob.n_z, 42, dtype=dt)        # generated on the GPU
+    ref = Reference(prob, workers=os.cpu_count() or 1)
+    assert np.array_equal(f, ref.random_field(42, c["dtype"]))  # device RNG == reference RNG
+    ug, rg = acg.solve(ctx, f, epsilon=1e-300, tau=1e-300, maxiter=c["iters"])
+    uo, ro = ref.solve(f, epsilon=1e-300, tau=1e-300, maxiter=c["iters"])
+    assert rg.iterations == ro.iterations == c["iters"]
+    for h in ("residual_history", "kappa_history", "alpha_history", "beta_history"):
+        assert np.array_equal(getattr(rg, h), getattr(ro, h)), h
+    assert rg.true_residual == ro.true_residual
+    assert np.array_equal(ug, uo)
+    # size-independent: u is finite and the recurrence residual matches ||f - A u||
+    assert np.isfinite(ug).all()
+    assert abs(rg.true_residual - rg.residual_history[-1]) <= 1e-6 * rg.residual_history[0]
