@@ -45,6 +45,8 @@ struct SlabView {
     const T* prof;    // kProfRows x n_z
     const T* col;     // kColRows x (m_loc * m)
     int tm_ok;        // host side: the TMEM Thomas sweep's division ranges hold (k_validate_tm)
+    int plane_begin = 0;  // fused stencil sweep only: planes [plane_begin, plane_begin + plane_count)
+    int plane_count = 0;  // (0: all m_loc planes); see spmv_plane_ranges
 };
 
 // Reasons a solve stops with NumericalBreakdown (operator.hpp:21-24,
@@ -129,6 +131,10 @@ bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st);
 template <typename T>
 void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scalars<T>* S,
                          const Scalars<T>* gate, T* phi_scratch, cudaStream_t st);
+// Can launch_fused_spmv sweep a sub-range of the slab's planes (halo overlap:
+// interior planes while the ghost planes are in flight, then the boundary)?
+template <typename T>
+bool spmv_plane_ranges(const SlabView<T>& v, bool fast);
 template <typename T>
 int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
                       const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin = nullptr);

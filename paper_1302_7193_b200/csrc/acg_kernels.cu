@@ -1236,15 +1236,12 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
     post_launch("precondition");
 }
 
+// K2 variant: ACG_SPMV=plain|ring|tile|pair|pair2 overrides; default: the
+// two-column kernels (the tile kernel for odd m) — fp64 with every stencil
+// input in the cp.async ring (C3 K2 1.18 ms), fp32 with the neighbour rows
+// loaded a level ahead (C4 K2 2.59 ms); measured.
 template <typename T>
-int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                      const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin) {
-    int leaves = 0;
-    const dim3 block(32, kStencilWarps);
-    const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
-    // ACG_SPMV=plain|ring|tile overrides the variant; ACG_SPMV_D the tile prefetch depth,
-    // ACG_SPMV_X the ring kernel's warps along j.
-    // Default: the cp.async ring for fp64, shared z tiles for fp32 (measured, C3 / C4).
+int spmv_mode() {
     static const int mode = [] {
         const char* e = std::getenv("ACG_SPMV");
         if (e && std::string(e) == "plain") return 1;
@@ -1252,11 +1249,25 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         if (e && std::string(e) == "tile") return 0;
         if (e && std::string(e) == "pair") return 5;
         if (e && std::string(e) == "pair2") return 6;
-        // two-column kernels (the tile kernel for odd m): fp64 with every stencil
-        // input in the cp.async ring (C3 K2 1.18 ms), fp32 with the neighbour rows
-        // loaded a level ahead (C4 K2 2.59 ms); measured.
         return sizeof(T) == 4 ? 5 : 6;
     }();
+    return mode;
+}
+
+template <typename T>
+bool spmv_plane_ranges(const SlabView<T>& v, bool fast) {
+    (void)fast;
+    const int mode = spmv_mode<T>();
+    return (mode == 5 || mode == 6) && v.m % 2 == 0;
+}
+
+template <typename T>
+int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
+                      const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin) {
+    int leaves = 0;
+    const dim3 block(32, kStencilWarps);
+    const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
+    const int mode = spmv_mode<T>();
     static const int pair_cfg = [] {  // ACG_SPMV_PAIR = 10*D + min CTAs per SM
         const char* e = std::getenv("ACG_SPMV_PAIR");
         return e ? std::atoi(e) : (sizeof(T) == 4 ? 23 : 32);
@@ -1280,7 +1291,8 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         T* stg = leaves ? stage : nullptr;
         const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                          static_cast<size_t>(Dp + 1) * 4 * 2 * 32 * kStencilWarps);
-        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps), v.m_loc);
+        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps),
+                      v.plane_count ? v.plane_count : v.m_loc);
 #define ACG_PR(F, DD, MB)                                                                         \
     do {                                                                                          \
         ensure_smem(k_fused_spmv_pair<T, F, DD, MB>, smem);                                       \
@@ -1304,7 +1316,8 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         T* stg = leaves ? stage : nullptr;
         const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                          static_cast<size_t>(Dp + 1) * 7 * 2 * 32 * kStencilWarps);
-        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps), v.m_loc);
+        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps),
+                      v.plane_count ? v.plane_count : v.m_loc);
         FinishDev<T> fd{nullptr, nullptr, -1};
         if (fin && leaves > 0 &&
             static_cast<size_t>(leaves) + 4 * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
@@ -1555,6 +1568,7 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
                                       Scalars<T>*, T*, T*, cudaStream_t, Finish<T>*);           \
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
                                          const Scalars<T>*, T*, cudaStream_t);                  \
+    template bool spmv_plane_ranges<T>(const SlabView<T>&, bool);                               \
     template int launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,       \
                                       const Scalars<T>*, T*, cudaStream_t, Finish<T>*);         \
     template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \

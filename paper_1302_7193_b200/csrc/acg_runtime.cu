@@ -285,6 +285,8 @@ struct acg_context {
     int nslabs_total = 1, rank = 0;
     acg_comm* comm = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t halo_stream = nullptr;       // ranks > 1: halo exchange beside the interior sweep
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     bool exact_tree = true;
     std::vector<Slab> slabs;  // local slabs (same device)
     void* gather = nullptr;       // nslabs_total * 4 T
@@ -599,6 +601,11 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
         CK(cudaMalloc(&c->gather_send, 4 * c->s));
         if (c->comm && c->comm->kind == 1 && p > 1)
             c->ipc = ipc_attach(c->comm, c->slabs[0].plane, c->s);
+        if (c->comm && p > 1) {
+            CK(cudaStreamCreateWithFlags(&c->halo_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+        }
         *out = c.release();
     });
 }
@@ -630,6 +637,9 @@ acg_status acg_context_destroy(acg_context* c) {
         if (c->gather) cudaFree(c->gather);
         if (c->gather_send) cudaFree(c->gather_send);
         ipc_detach(c->ipc.get());
+        if (c->halo_stream) cudaStreamDestroy(c->halo_stream);
+        if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+        if (c->ev_halo) cudaEventDestroy(c->ev_halo);
         if (c->stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -840,7 +850,8 @@ void download_dev_t(const acg_field* f, void* dev, acg_layout layout, acg_host_s
 // Ghost plane -1 of slab s <- plane m_loc-1 of slab s-1; ghost plane m_loc of
 // slab s <- plane 0 of slab s+1. Device copies between local slabs, NCCL
 // send/recv between ranks.
-void halo(const acg_context* c, const acg_field* f) {
+void halo(const acg_context* c, const acg_field* f, cudaStream_t hs = nullptr) {
+    if (!hs) hs = c->stream;
     if (c->nslabs_total == 1) return;
     const size_t pb = static_cast<size_t>(c->slabs[0].plane) * c->s;
     auto plane_ptr = [&](size_t si, int il) {
@@ -866,23 +877,23 @@ void halo(const acg_context* c, const acg_field* f) {
         unsigned long long* fl[2] = {nullptr, nullptr};
         if (r > 0) {  // my plane 0 is the ghost "from above" of rank r-1
             CK(cudaMemcpyAsync(ip.ghost(r - 1, par, 1), plane_ptr(0, 0), pb, cudaMemcpyDeviceToDevice,
-                               c->stream));
+                               hs));
             fl[0] = ip.flags(r - 1) + 1;
         }
         if (r + 1 < p) {  // my last plane is the ghost "from below" of rank r+1
             CK(cudaMemcpyAsync(ip.ghost(r + 1, par, 0), plane_ptr(0, m_loc - 1), pb,
-                               cudaMemcpyDeviceToDevice, c->stream));
+                               cudaMemcpyDeviceToDevice, hs));
             fl[1] = ip.flags(r + 1) + 0;
         }
-        launch_ipc_signal(fl, 2, seq, c->stream);
+        launch_ipc_signal(fl, 2, seq, hs);
         launch_ipc_wait(ip.flags(r), 2, (r > 0 ? 1ull : 0ull) | (r + 1 < p ? 2ull : 0ull), seq,
-                        c->stream);
+                        hs);
         if (r > 0)
             CK(cudaMemcpyAsync(plane_ptr(0, -1), ip.ghost(r, par, 0), pb, cudaMemcpyDeviceToDevice,
-                               c->stream));
+                               hs));
         if (r + 1 < p)
             CK(cudaMemcpyAsync(plane_ptr(0, m_loc), ip.ghost(r, par, 1), pb,
-                               cudaMemcpyDeviceToDevice, c->stream));
+                               cudaMemcpyDeviceToDevice, hs));
         return;
     }
     NcclApi& api = nccl();
@@ -892,13 +903,13 @@ void halo(const acg_context* c, const acg_field* f) {
     const size_t cnt = static_cast<size_t>(s.plane);
     nccl_check(api.groupStart(), "ncclGroupStart");
     if (r > 0) {
-        nccl_check(api.send(plane_ptr(0, 0), cnt, dt, r - 1, c->comm->comm, c->stream), "ncclSend");
-        nccl_check(api.recv(plane_ptr(0, -1), cnt, dt, r - 1, c->comm->comm, c->stream), "ncclRecv");
+        nccl_check(api.send(plane_ptr(0, 0), cnt, dt, r - 1, c->comm->comm, hs), "ncclSend");
+        nccl_check(api.recv(plane_ptr(0, -1), cnt, dt, r - 1, c->comm->comm, hs), "ncclRecv");
     }
     if (r + 1 < p) {
-        nccl_check(api.send(plane_ptr(0, s.m_loc - 1), cnt, dt, r + 1, c->comm->comm, c->stream),
+        nccl_check(api.send(plane_ptr(0, s.m_loc - 1), cnt, dt, r + 1, c->comm->comm, hs),
                    "ncclSend");
-        nccl_check(api.recv(plane_ptr(0, s.m_loc), cnt, dt, r + 1, c->comm->comm, c->stream),
+        nccl_check(api.recv(plane_ptr(0, s.m_loc), cnt, dt, r + 1, c->comm->comm, hs),
                    "ncclRecv");
     }
     nccl_check(api.groupEnd(), "ncclGroupEnd");
@@ -1579,16 +1590,43 @@ void iterate_interleaved(acg_solver* s) {
     if (!fin1.used) reduce<T>(c, 2, kOpIlPrec, S, nullptr, true, &leaves);
     s->timer.end(kFusedPrec);
     s->timer.begin(kFusedSpmv);
-    halo(c, s->z);
     Finish<T> fin2{S[0], c->slabs[0].fin_counter, kOpIlSpmv, false};
-    for (size_t si = 0; si < c->slabs.size(); ++si) {
+    auto spmv = [&](size_t si, int pb, int pc, Finish<T>* f) {
+        SlabView<T> v = view<T>(c, si);
+        v.plane_begin = pb;
+        v.plane_count = pc;
+        return launch_fused_spmv<T>(
+            v, c->fast(), static_cast<T*>(s->u->data(si)), static_cast<T*>(s->p->data(si)),
+            static_cast<T*>(s->q->data(si)), static_cast<const T*>(s->z->data(si)),
+            static_cast<T*>(c->slabs[si].part[0]), S[si], static_cast<T*>(c->slabs[si].stage),
+            c->stream, f);
+    };
+    static const bool overlap_on = [] {
+        const char* e = std::getenv("ACG_HALO_OVERLAP");
+        return !(e && std::string(e) == "0");
+    }();
+    const int m_loc0 = c->slabs[0].m_loc;
+    if (c->halo_stream && overlap_on && m_loc0 >= 3 &&
+        spmv_plane_ranges<T>(view<T>(c, 0), c->fast())) {
+        // ranks > 1: the ghost planes travel on the halo stream while the interior
+        // planes (which never read a ghost) are swept; the two boundary planes follow
+        CK(cudaEventRecord(c->ev_ready, c->stream));
+        CK(cudaStreamWaitEvent(c->halo_stream, c->ev_ready, 0));
+        halo(c, s->z, c->halo_stream);
+        CK(cudaEventRecord(c->ev_halo, c->halo_stream));
         s->ktimer.begin(kFusedSpmv);
-        leaves[si] = launch_fused_spmv<T>(
-            view<T>(c, si), c->fast(), static_cast<T*>(s->u->data(si)),
-            static_cast<T*>(s->p->data(si)), static_cast<T*>(s->q->data(si)),
-            static_cast<const T*>(s->z->data(si)), static_cast<T*>(c->slabs[si].part[0]), S[si],
-            static_cast<T*>(c->slabs[si].stage), c->stream, single ? &fin2 : nullptr);
+        leaves[0] = spmv(0, 1, m_loc0 - 2, nullptr);
+        CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+        spmv(0, 0, 1, nullptr);
+        spmv(0, m_loc0 - 1, 1, nullptr);
         s->ktimer.end(kFusedSpmv);
+    } else {
+        halo(c, s->z);
+        for (size_t si = 0; si < c->slabs.size(); ++si) {
+            s->ktimer.begin(kFusedSpmv);
+            leaves[si] = spmv(si, 0, 0, single ? &fin2 : nullptr);
+            s->ktimer.end(kFusedSpmv);
+        }
     }
     if (!fin2.used) reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true, &leaves);
     s->timer.end(kFusedSpmv);

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     const int tid = threadIdx.y * 32 + threadIdx.x;
     load_profile(prof, v.prof, 4 * n_z, tid, NT);
     __syncthreads();
-    const int il = blockIdx.y;
+    const int il = v.plane_begin + blockIdx.y;
     const int jr = blockIdx.x * 2 * NT + 2 * tid;
     const bool valid = jr < m;  // m even: both columns exist
     if (stage == nullptr && !valid) return;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     const int tid = threadIdx.y * 32 + threadIdx.x;
     load_profile(prof, v.prof, 4 * n_z, tid, NT);
     __syncthreads();
-    const int il = blockIdx.y;
+    const int il = v.plane_begin + blockIdx.y;
     const int jr = blockIdx.x * 2 * NT + 2 * tid;
     const bool valid = jr < m;  // m even: both columns exist
     if (stage == nullptr && !valid) return;
