@@ -168,13 +168,24 @@ void launch_fill_random(const SlabView<T>& v, uint64_t seed, T* x, cudaStream_t 
 template <typename T>
 void launch_tree_stage1(const TreePlan& plan, const T* in0, const T* in1, const T* in2, int nv,
                         T* stage, const Scalars<T>* gate, cudaStream_t st);
+// Peer-memory ranks: stage 2 also copies the rank's 4 slab sums into every
+// rank's mailbox (dst[q] + rank*4) and releases flag[q][rank] = seq.
+template <typename T>
+struct IpcPut {
+    T* const* dst;
+    unsigned long long* const* flag;
+    int n, rank;
+    unsigned long long seq;
+};
 template <typename T>
 void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
                         bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
-                        cudaStream_t st);
+                        cudaStream_t st, const IpcPut<T>* put = nullptr);
+// wait_flags (peer-memory ranks): first wait until wait_flags[q] >= seq for all q < nslabs
 template <typename T>
 void launch_finish(const T* gather, int nv, int nslabs, bool exact_tree, Scalars<T>* S, int op,
-                   cudaStream_t st);
+                   cudaStream_t st, const unsigned long long* wait_flags = nullptr,
+                   unsigned long long seq = 0);
 
 // Peer-memory (CUDA IPC) transport between the ranks of one node. Flags are
 // 64-bit sequence numbers in the owner's mailbox, written by peers with
@@ -186,11 +197,6 @@ void launch_ipc_signal(unsigned long long* const* flags, int n, unsigned long lo
                        cudaStream_t st);
 void launch_ipc_wait(const unsigned long long* flags, int n, unsigned long long need,
                      unsigned long long seq, cudaStream_t st);
-// every rank's 4 slab sums: src (4 T) -> dst[q] + rank*4 for q < n, then
-// flag[q] (in rank q's mailbox) = seq; dst and flag are device arrays of n pointers
-template <typename T>
-void launch_ipc_put_sums(const T* src, T* const* dst, unsigned long long* const* flag, int n,
-                         int rank, unsigned long long seq, cudaStream_t st);
 
 // relayout between the reference's host layouts and plane-major (K7):
 // out[x*osx + y + b*osb] = in[x + y*isy + b*isb]  for x<nx, y<ny, b<nb

@@ -784,11 +784,30 @@ __global__ void __launch_bounds__(1024)
 // Stage 2 with warp shuffles: NTH threads, C consecutive leaves each (perfect
 // tree in registers), then a shuffle tree per warp and a perfect tree over the
 // warps — the same perfect tree over nleaves = NTH * C leaves as k_tree2.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <typename T, int C>
 __global__ void __launch_bounds__(256)
     k_tree2_shfl(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather,
-                 int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op) {
-    if (op != kOpStore && S->done) return;
+                 int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op,
+                 const IpcPut<T> put) {
+    // peer-memory ranks: the slab sums go straight into every rank's mailbox
+    // (put.n > 0). The put is unconditional (a finished solve still keeps the
+    // ranks' flag sequence in step), the reduction itself is gated.
+    if (op != kOpStore && S->done) {
+        if (put.n > 0 && threadIdx.x == 0) {
+            __threadfence_system();
+            for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+        }
+        return;
+    }
     __shared__ T wsum[3][8];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -824,11 +843,29 @@ __global__ void __launch_bounds__(256)
             run_op(S, op, sums);
         }
     }
+    if (put.n > 0 && tid == 0) {  // rank `put.rank`'s 4 sums into every mailbox, then the flags
+        for (int q = 0; q < put.n; ++q) {
+            T* d = put.dst[q] + put.rank * 4;
+            for (int a = 0; a < 4; ++a) d[a] = gather[slab * 4 + a];
+        }
+        __threadfence_system();
+        for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+    }
 }
 
 template <typename T>
 __global__ void k_finish(const T* __restrict__ gather, int nv, int nslabs, int exact,
-                         Scalars<T>* __restrict__ S, int op) {
+                         Scalars<T>* __restrict__ S, int op, const unsigned long long* wait_flags,
+                         unsigned long long seq) {
+    if (wait_flags) {  // peer-memory ranks: every rank's sums have landed in this mailbox
+        const long long t0 = clock64();
+        for (int q = 0; q < nslabs; ++q)
+            while (ld_acquire_sys(wait_flags + q) < seq) {
+                if (clock64() - t0 > (40ll << 30)) __trap();
+                __nanosleep(32);
+            }
+        __threadfence_system();
+    }
     if (op != kOpStore && S->done) return;
     T sums[4] = {T(0), T(0), T(0), T(0)};
     for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
@@ -836,14 +873,6 @@ __global__ void k_finish(const T* __restrict__ gather, int nv, int nslabs, int e
 }
 
 // ------------------------------------------------------- peer-memory transport
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 struct FlagPtrs {
     unsigned long long* f[8];
@@ -868,18 +897,6 @@ __global__ void k_ipc_wait(const unsigned long long* flags, int n, unsigned long
     __threadfence_system();
 }
 
-template <typename T>
-__global__ void k_ipc_put_sums(const T* __restrict__ src, T* const* __restrict__ dst,
-                               unsigned long long* const* __restrict__ flag, int n, int rank,
-                               unsigned long long seq) {
-    const int q = threadIdx.x;
-    if (q < n) {
-        T* d = dst[q] + rank * 4;
-        for (int a = 0; a < 4; ++a) d[a] = src[a];
-        __threadfence_system();
-        st_release_sys(flag[q] + rank, seq);
-    }
-}
 
 // --------------------------------------------------------- launch helpers
 inline void post_launch(const char* what) {
@@ -1496,24 +1513,25 @@ void launch_tree_stage1(const TreePlan& plan, const T* in0, const T* in1, const 
 template <typename T>
 void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
                         bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
-                        cudaStream_t st) {
+                        cudaStream_t st, const IpcPut<T>* put) {
+    const IpcPut<T> pp = put ? *put : IpcPut<T>{nullptr, nullptr, 0, 0, 0};
     const int nl = plan.blocks;  // power of two
     static const bool legacy = [] {
         const char* e = std::getenv("ACG_TREE2");
         return e && std::string(e) == "legacy";
     }();
-    if (!legacy && nl <= 256 * 64) {
+    if ((!legacy || pp.n > 0) && nl <= 256 * 64) {
         const int c = nl > 256 ? nl / 256 : 1;
         const int nt = nl / c;
         const int f = finish ? 1 : 0, ex = exact_tree ? 1 : 0;
         switch (c) {
-            case 1: k_tree2_shfl<T, 1><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
-            case 2: k_tree2_shfl<T, 2><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
-            case 4: k_tree2_shfl<T, 4><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
-            case 8: k_tree2_shfl<T, 8><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
-            case 16: k_tree2_shfl<T, 16><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
-            case 32: k_tree2_shfl<T, 32><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
-            default: k_tree2_shfl<T, 64><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op); break;
+            case 1: k_tree2_shfl<T, 1><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 2: k_tree2_shfl<T, 2><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 4: k_tree2_shfl<T, 4><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 8: k_tree2_shfl<T, 8><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 16: k_tree2_shfl<T, 16><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 32: k_tree2_shfl<T, 32><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            default: k_tree2_shfl<T, 64><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
         }
         post_launch("tree2");
         return;
@@ -1526,8 +1544,8 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
 
 template <typename T>
 void launch_finish(const T* gather, int nv, int nslabs, bool exact_tree, Scalars<T>* S, int op,
-                   cudaStream_t st) {
-    k_finish<T><<<1, 1, 0, st>>>(gather, nv, nslabs, exact_tree ? 1 : 0, S, op);
+                   cudaStream_t st, const unsigned long long* wait_flags, unsigned long long seq) {
+    k_finish<T><<<1, 1, 0, st>>>(gather, nv, nslabs, exact_tree ? 1 : 0, S, op, wait_flags, seq);
     post_launch("finish");
 }
 
@@ -1545,12 +1563,6 @@ void launch_ipc_wait(const unsigned long long* flags, int n, unsigned long long 
     post_launch("ipc_wait");
 }
 
-template <typename T>
-void launch_ipc_put_sums(const T* src, T* const* dst, unsigned long long* const* flag, int n,
-                         int rank, unsigned long long seq, cudaStream_t st) {
-    k_ipc_put_sums<T><<<1, 64, 0, st>>>(src, dst, flag, n, rank, seq);
-    post_launch("ipc_put_sums");
-}
 
 template <typename T>
 void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy, long long isb,
@@ -1586,10 +1598,9 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
     template void launch_tree_stage1<T>(const TreePlan&, const T*, const T*, const T*, int, T*, \
                                         const Scalars<T>*, cudaStream_t);                       \
     template void launch_tree_stage2<T>(const TreePlan&, const T*, int, T*, int, bool, int,     \
-                                        bool, Scalars<T>*, int, cudaStream_t);                  \
-    template void launch_finish<T>(const T*, int, int, bool, Scalars<T>*, int, cudaStream_t);   \
-    template void launch_ipc_put_sums<T>(const T*, T* const*, unsigned long long* const*, int,   \
-                                         int, unsigned long long, cudaStream_t);                 \
+                                        bool, Scalars<T>*, int, cudaStream_t, const IpcPut<T>*); \
+    template void launch_finish<T>(const T*, int, int, bool, Scalars<T>*, int, cudaStream_t,    \
+                                   const unsigned long long*, unsigned long long);              \
     template void launch_transpose<T>(const T*, T*, int, int, int, long long, long long,        \
                                       long long, long long, cudaStream_t);
 

@@ -925,6 +925,21 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
             const Scalars<T>* gate_or_null, bool gated, const std::vector<int>* leaves = nullptr) {
     const bool single = c->nslabs_total == 1;
     T* gather = static_cast<T*>(c->gather);
+    // peer memory: stage 2 puts the slab sums into every mailbox, the finish waits for them
+    IpcPut<T> put{nullptr, nullptr, 0, 0, 0};
+    unsigned long long seq = 0;
+    int par = 0;
+    if (c->ipc && !single) {
+        IpcState& ip = *c->ipc;
+        seq = ++ip.red_seq;
+        par = static_cast<int>(seq & 1);
+        put.dst = static_cast<T* const*>(ip.dptr) + static_cast<size_t>(par) * ip.p;
+        put.flag = reinterpret_cast<unsigned long long* const*>(static_cast<void* const*>(ip.dptr) +
+                                                                2 * ip.p);
+        put.n = ip.p;
+        put.rank = ip.rank;
+        put.seq = seq;
+    }
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& s = c->slabs[si];
         const Scalars<T>* gate = gated ? (gate_or_null ? gate_or_null : S[si]) : nullptr;
@@ -940,20 +955,14 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
         T* g = c->comm ? static_cast<T*>(c->gather_send) : gather;
         const int slot = c->comm ? 0 : s.index;
         launch_tree_stage2<T>(plan, static_cast<const T*>(s.stage), nv, g, slot, single,
-                              c->nslabs_total, c->exact_tree, S[si], op, c->stream);
+                              c->nslabs_total, c->exact_tree, S[si], op, c->stream,
+                              put.n ? &put : nullptr);
     }
     if (single) return;
-    if (c->ipc) {  // peer memory: every rank's slab sums into every mailbox
+    const unsigned long long* wait_flags = nullptr;
+    if (c->ipc) {
         IpcState& ip = *c->ipc;
-        const unsigned long long seq = ++ip.red_seq;
-        const int par = static_cast<int>(seq & 1);
-        T* const* dst = static_cast<T* const*>(ip.dptr) + static_cast<size_t>(par) * ip.p;
-        unsigned long long* const* fl =
-            reinterpret_cast<unsigned long long* const*>(static_cast<void* const*>(ip.dptr) + 2 * ip.p);
-        launch_ipc_put_sums<T>(static_cast<const T*>(c->gather_send), dst, fl, ip.p, ip.rank, seq,
-                               c->stream);
-        launch_ipc_wait(ip.flags(ip.rank) + 2, ip.p, ip.p >= 64 ? ~0ull : ((1ull << ip.p) - 1), seq,
-                        c->stream);
+        wait_flags = ip.flags(ip.rank) + 2;
         gather = reinterpret_cast<T*>(ip.gather(ip.rank, par, c->s));
     } else if (c->comm) {
         const ncclDataType_t dt = c->dtype == ACG_F32 ? ncclFloat32 : ncclFloat64;
@@ -961,7 +970,8 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
                    "ncclAllGather");
     }
     for (size_t si = 0; si < c->slabs.size(); ++si)
-        launch_finish<T>(gather, nv, c->nslabs_total, c->exact_tree, S[si], op, c->stream);
+        launch_finish<T>(gather, nv, c->nslabs_total, c->exact_tree, S[si], op, c->stream,
+                         wait_flags, seq);
 }
 
 template <typename T>
