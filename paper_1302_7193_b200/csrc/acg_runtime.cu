@@ -219,7 +219,7 @@ std::unique_ptr<IpcState> ipc_attach(acg_comm* comm, long long plane, size_t s) 
         CK(cudaIpcOpenMemHandle(&ptr, r.handle, cudaIpcMemLazyEnablePeerAccess));
         st->peer[q] = static_cast<char*>(ptr);
     }
-    // device pointer tables for k_ipc_put_sums
+    // device pointer tables for the stage-2 put (IpcPut: sums destinations, flags)
     std::vector<void*> tab(3 * static_cast<size_t>(p));
     for (int par = 0; par < 2; ++par)
         for (int q = 0; q < p; ++q) tab[par * p + q] = st->gather(q, par, s);
