@@ -255,7 +255,7 @@ def run_gpu(args, cfg):
     barrier()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    solver.time_kernels(True)
+    solver.time_kernels(not args.no_ktime)
     launches_before = capi.launch_count()
     with ClockSampler(dev) as clk:
         ev0.record(stream)
@@ -405,6 +405,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ktime", action="store_true",
+                    help="no per-launch K1/K2 events inside the timed region (overhead check)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "acg_internal.h"
 
@@ -64,6 +65,45 @@ __device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
 __device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// Programmatic dependent launch: kernels launched with the PDL attribute may
+// start while the previous kernel of the stream finishes; they must wait for it
+// (griddepcontrol.wait, a no-op without the attribute) before reading its
+// outputs. launch_dependents lets the next kernel's CTAs be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+// Reads of the device scalars a PDL kernel makes after pdl_wait(): the scalars
+// are written by the immediately preceding kernel, so they must not come from
+// a load the compiler hoisted above the wait (a const __restrict__ pointer is
+// otherwise read through the non-coherent path, before griddepcontrol.wait).
+template <typename V>
+__device__ __forceinline__ V ld_dep(const V* p) {
+    return *reinterpret_cast<const volatile V*>(p);
+}
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ACG_PDL");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline int grid_1d(long long n, int threads) {
     long long b = (n + threads - 1) / threads;
@@ -798,6 +838,8 @@ __global__ void __launch_bounds__(256)
     k_tree2_shfl(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather,
                  int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op,
                  const IpcPut<T> put) {
+    pdl_trigger();  // the next sweep may start its prologue while this tree runs
+    pdl_wait();
     // peer-memory ranks: the slab sums go straight into every rank's mailbox
     // (put.n > 0). The put is unconditional (a finished solve still keeps the
     // ranks' flag sequence in step), the reduction itself is gated.
@@ -1027,8 +1069,8 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
         fin->used = true;
     }
     ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
-    k_thomas_tm<T, Fast, Fused, C><<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, tcols,
-                                                             leaves ? stage : nullptr, leaves, fd);
+    launch_pdl(k_thomas_tm<T, Fast, Fused, C>, grid, block, smem, st, v, r, in, out, p2, pk,
+               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, fd);
     return leaves;
 }
 
@@ -1344,7 +1386,7 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
 #define ACG_PR(F, DD, MB)                                                                         \
     do {                                                                                          \
         ensure_smem(k_fused_spmv_pair2<T, F, DD, MB>, smem);                                      \
-        k_fused_spmv_pair2<T, F, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves, fd); \
+        launch_pdl(k_fused_spmv_pair2<T, F, DD, MB>, g2, block, smem, st, v, u, p, q, z, part, S, stg, leaves, fd); \
     } while (0)
         switch (fast ? -pair_cfg : pair_cfg) {
             case 22: ACG_PR(false, 2, 2); break;
@@ -1525,13 +1567,13 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
         const int nt = nl / c;
         const int f = finish ? 1 : 0, ex = exact_tree ? 1 : 0;
         switch (c) {
-            case 1: k_tree2_shfl<T, 1><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
-            case 2: k_tree2_shfl<T, 2><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
-            case 4: k_tree2_shfl<T, 4><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
-            case 8: k_tree2_shfl<T, 8><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
-            case 16: k_tree2_shfl<T, 16><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
-            case 32: k_tree2_shfl<T, 32><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
-            default: k_tree2_shfl<T, 64><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 1: launch_pdl(k_tree2_shfl<T, 1>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 2: launch_pdl(k_tree2_shfl<T, 2>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 4: launch_pdl(k_tree2_shfl<T, 4>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 8: launch_pdl(k_tree2_shfl<T, 8>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 16: launch_pdl(k_tree2_shfl<T, 16>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 32: launch_pdl(k_tree2_shfl<T, 32>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            default: launch_pdl(k_tree2_shfl<T, 64>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
         }
         post_launch("tree2");
         return;

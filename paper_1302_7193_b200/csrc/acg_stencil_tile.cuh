@@ -285,13 +285,14 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     using A = Ar<T, Fast>;
     using P = Pair<T>;
     constexpr int NT = 32 * kStencilWarps, NS = D + 1;
-    if (S->done) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* prof = reinterpret_cast<T*>(smem_raw);
     const int n_z = v.n_z, m = v.m;
     const int tid = threadIdx.y * 32 + threadIdx.x;
-    load_profile(prof, v.prof, 4 * n_z, tid, NT);
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);  // static data: before the dependency wait
     __syncthreads();
+    pdl_wait();  // programmatic dependent launch: the previous grid has completed
+    if (ld_dep(&S->done)) return;  // block-uniform
     const int il = v.plane_begin + blockIdx.y;
     const int jr = blockIdx.x * 2 * NT + 2 * tid;
     const bool valid = jr < m;  // m even: both columns exist
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     const T* dP = prof + kProfD * n_z;
     const Col<T> ca = load_col(v, il, j);
     const Col<T> cb = load_col(v, il, j + 1);
-    const T alpha = S->alpha, beta = S->beta;
+    const T alpha = ld_dep(&S->alpha), beta = ld_dep(&S->beta);
     const long long base = static_cast<long long>(il) * v.plane + j;
     const T* zc = z + base;
     T* uc = u + base;
