@@ -38,6 +38,24 @@ enum ColRow { kColArea = 0,  // |T|
               kColInvA = 7,  // 1 / |T|          (fast math only)
               kColRows = 8 };
 
+// Peer-memory halo fused into the interleaved sweeps (IPC transport, ranks > 1,
+// DESIGN.md §6). Producer (K1, k_thomas_tm): the CTAs of plane 0 / plane m_loc-1
+// also store their z columns into the neighbour's mailbox slot and the last CTA
+// of the plane releases the neighbour's flag. Consumer (K2, k_fused_spmv_pair2):
+// the CTAs of the boundary planes acquire the flag and read the ghost rows from
+// this rank's mailbox. Side 0 = toward rank r-1 (plane 0 / ghost plane -1),
+// side 1 = toward rank r+1 (plane m_loc-1 / ghost plane m_loc).
+template <typename T>
+struct HaloLink {
+    T* put[2] = {nullptr, nullptr};                        // neighbour's mailbox slot
+    unsigned long long* put_flag[2] = {nullptr, nullptr};  // neighbour's flag
+    unsigned* arrive = nullptr;                            // [2] CTA arrivals (zero at rest)
+    const T* ghost[2] = {nullptr, nullptr};                // own mailbox slots
+    const unsigned long long* wait_flag[2] = {nullptr, nullptr};
+    unsigned long long seq = 0;
+    int on = 0;
+};
+
 template <typename T>
 struct SlabView {
     int m, n_z, m_loc, i0;
@@ -47,6 +65,7 @@ struct SlabView {
     int tm_ok;        // host side: the TMEM Thomas sweep's division ranges hold (k_validate_tm)
     int plane_begin = 0;  // fused stencil sweep only: planes [plane_begin, plane_begin + plane_count)
     int plane_count = 0;  // (0: all m_loc planes); see spmv_plane_ranges
+    HaloLink<T> halo;     // fused peer-memory halo (fused_halo_ok); off by default
 };
 
 // Reasons a solve stops with NumericalBreakdown (operator.hpp:21-24,
@@ -133,6 +152,10 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
                          const Scalars<T>* gate, T* phi_scratch, cudaStream_t st);
 // Can launch_fused_spmv sweep a sub-range of the slab's planes (halo overlap:
 // interior planes while the ghost planes are in flight, then the boundary)?
+// true when the interleaved sweeps chosen for this view honour SlabView::halo
+// (K1 = k_thomas_tm default configuration, K2 = k_fused_spmv_pair2).
+template <typename T>
+bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm);
 template <typename T>
 bool spmv_plane_ranges(const SlabView<T>& v, bool fast);
 template <typename T>

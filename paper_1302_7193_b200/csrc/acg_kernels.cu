@@ -81,6 +81,29 @@ __device__ __forceinline__ V ld_dep(const V* p) {
     return *reinterpret_cast<const volatile V*>(p);
 }
 
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Fused halo, consumer side: thread 0 acquires the neighbour's flag (set by its
+// K1 after the boundary plane landed in this rank's mailbox), then the CTA
+// proceeds. Traps after ~20 s instead of hanging when a peer never arrives.
+__device__ __forceinline__ void halo_acquire(const unsigned long long* flag, unsigned long long seq) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire_sys(flag) < seq) {
+            if (clock64() - t0 > (40ll << 30)) __trap();
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("ACG_PDL");
@@ -824,14 +847,6 @@ __global__ void __launch_bounds__(1024)
 // Stage 2 with warp shuffles: NTH threads, C consecutive leaves each (perfect
 // tree in registers), then a shuffle tree per warp and a perfect tree over the
 // warps — the same perfect tree over nleaves = NTH * C leaves as k_tree2.
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 template <typename T, int C>
 __global__ void __launch_bounds__(256)
@@ -1200,6 +1215,14 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
                   Finish<T>* fin = nullptr) {
     const int tmc = thomas_tm_choice();
     const int tm2 = thomas_tm2_choice<T>();
+    if (v.halo.on) {  // fused halo (fused_halo_ok): the default TMEM sweep carries the planes
+        if (tmc == 0 || !v.tm_ok || phi_scratch != nullptr || thomas_tm_cols(v.n_z, sizeof(T)) > 256) {
+            std::fprintf(stderr, "acg: fused halo requested for a sweep that cannot carry it\n");
+            std::abort();
+        }
+        return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmCfg<4, 15, 15>>(v, r, in, out, p2, pk, S,
+                                                                          gate, stage, st, fin);
+    }
     if (tm2 != 0 && tmc != 0 && v.tm_ok && phi_scratch == nullptr && !thomas_tma_enabled()) {
         int l = -1;
         l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Cfg<4, 15, 15>>(v, r, in, out, p2, pk, S,
@@ -1314,6 +1337,17 @@ int spmv_mode() {
 }
 
 template <typename T>
+bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
+    (void)fast;
+    static const bool off = [] {  // ACG_FUSED_HALO=0: copy + signal kernels instead (A/B)
+        const char* e = std::getenv("ACG_FUSED_HALO");
+        return e && std::string(e) == "0";
+    }();
+    return !off && thomas_tm_choice() != 0 && v.tm_ok && !phi_in_hbm &&
+           thomas_tm_cols(v.n_z, sizeof(T)) <= 256 && spmv_mode<T>() == 6 && v.m % 2 == 0;
+}
+
+template <typename T>
 bool spmv_plane_ranges(const SlabView<T>& v, bool fast) {
     (void)fast;
     const int mode = spmv_mode<T>();
@@ -1327,6 +1361,10 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
     const dim3 block(32, kStencilWarps);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
     const int mode = spmv_mode<T>();
+    if (v.halo.on && !(mode == 6 && v.m % 2 == 0 && v.plane_count == 0)) {
+        std::fprintf(stderr, "acg: fused halo requested for a stencil sweep that cannot carry it\n");
+        std::abort();
+    }
     static const int pair_cfg = [] {  // ACG_SPMV_PAIR = 10*D + min CTAs per SM
         const char* e = std::getenv("ACG_SPMV_PAIR");
         return e ? std::atoi(e) : (sizeof(T) == 4 ? 23 : 32);
@@ -1623,6 +1661,7 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
                                          const Scalars<T>*, T*, cudaStream_t);                  \
     template bool spmv_plane_ranges<T>(const SlabView<T>&, bool);                               \
+    template bool fused_halo_ok<T>(const SlabView<T>&, bool, bool);                              \
     template int launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,       \
                                       const Scalars<T>*, T*, cudaStream_t, Finish<T>*);         \
     template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \

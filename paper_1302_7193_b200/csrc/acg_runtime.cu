@@ -138,6 +138,7 @@ struct IpcState {
     size_t bytes = 0, plane_bytes = 0, off_ghost = 0, off_gather = 0;
     std::vector<char*> peer;  // mailbox of every rank (own = mbox)
     void* dptr = nullptr;     // device: T* sums_dst[2][p], u64* red_flag[p]
+    unsigned* arrive = nullptr;  // device [2]: fused-halo CTA arrival counters (HaloLink)
     unsigned long long halo_seq = 0, red_seq = 0;
     std::string file;
     unsigned long long* flags(int q) const { return reinterpret_cast<unsigned long long*>(peer[q]); }
@@ -224,6 +225,8 @@ std::unique_ptr<IpcState> ipc_attach(acg_comm* comm, long long plane, size_t s) 
     for (int par = 0; par < 2; ++par)
         for (int q = 0; q < p; ++q) tab[par * p + q] = st->gather(q, par, s);
     for (int q = 0; q < p; ++q) tab[2 * p + q] = st->flags(q) + 2;
+    CK(cudaMalloc(&st->arrive, 2 * sizeof(unsigned)));
+    CK(cudaMemset(st->arrive, 0, 2 * sizeof(unsigned)));
     CK(cudaMalloc(&st->dptr, tab.size() * sizeof(void*)));
     CK(cudaMemcpy(st->dptr, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
     return st;
@@ -234,6 +237,7 @@ void ipc_detach(IpcState* st) {
     for (int q = 0; q < st->p; ++q)
         if (q != st->rank && st->peer[q]) cudaIpcCloseMemHandle(st->peer[q]);
     if (st->dptr) cudaFree(st->dptr);
+    if (st->arrive) cudaFree(st->arrive);
     if (st->mbox) cudaFree(st->mbox);
     if (!st->file.empty()) unlink(st->file.c_str());
 }
@@ -1584,13 +1588,42 @@ void iterate_interleaved(acg_solver* s) {
         return e && std::string(e) == "1";
     }();
     const bool single = c->nslabs_total == 1 && cta_finish;
+    // Peer-memory halo fused into the sweeps: K1 stores its boundary
+    // planes into the neighbours' mailboxes and releases their flags; K2's boundary
+    // CTAs acquire them and read the ghost rows from the local mailbox. No copy or
+    // signal launches, no second stream.
+    HaloLink<T> hl;
+    if (c->ipc && c->slabs.size() == 1 &&
+        fused_halo_ok<T>(view<T>(c, 0), c->fast(), c->slabs[0].phi != nullptr)) {
+        IpcState& ip = *c->ipc;
+        const int r = ip.rank, p = ip.p;
+        const unsigned long long seq = ++ip.halo_seq;
+        const int par = static_cast<int>(seq & 1);
+        hl.on = 1;
+        hl.seq = seq;
+        hl.arrive = ip.arrive;
+        if (r > 0) {  // plane 0 <-> rank r-1 (its ghost "from above"; mine "from below")
+            hl.put[0] = reinterpret_cast<T*>(ip.ghost(r - 1, par, 1));
+            hl.put_flag[0] = ip.flags(r - 1) + 1;
+            hl.ghost[0] = reinterpret_cast<const T*>(ip.ghost(r, par, 0));
+            hl.wait_flag[0] = ip.flags(r) + 0;
+        }
+        if (r + 1 < p) {  // plane m_loc-1 <-> rank r+1
+            hl.put[1] = reinterpret_cast<T*>(ip.ghost(r + 1, par, 0));
+            hl.put_flag[1] = ip.flags(r + 1) + 0;
+            hl.ghost[1] = reinterpret_cast<const T*>(ip.ghost(r, par, 1));
+            hl.wait_flag[1] = ip.flags(r) + 1;
+        }
+    }
     Finish<T> fin1{S[0], c->slabs[0].fin_counter, kOpIlPrec, false};
     s->timer.begin(kFusedPrec);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& sl = c->slabs[si];
+        SlabView<T> v1 = view<T>(c, si);
+        v1.halo = hl;
         s->ktimer.begin(kFusedPrec);
         leaves[si] = launch_fused_prec<T>(
-            view<T>(c, si), c->fast(), static_cast<T*>(s->r->data(si)),
+            v1, c->fast(), static_cast<T*>(s->r->data(si)),
             static_cast<T*>(s->z->data(si)), static_cast<const T*>(s->q->data(si)),
             static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), S[si],
             static_cast<T*>(sl.phi), static_cast<T*>(sl.stage), c->stream,
@@ -1605,6 +1638,7 @@ void iterate_interleaved(acg_solver* s) {
         SlabView<T> v = view<T>(c, si);
         v.plane_begin = pb;
         v.plane_count = pc;
+        v.halo = hl;
         return launch_fused_spmv<T>(
             v, c->fast(), static_cast<T*>(s->u->data(si)), static_cast<T*>(s->p->data(si)),
             static_cast<T*>(s->q->data(si)), static_cast<const T*>(s->z->data(si)),
@@ -1616,7 +1650,11 @@ void iterate_interleaved(acg_solver* s) {
         return !(e && std::string(e) == "0");
     }();
     const int m_loc0 = c->slabs[0].m_loc;
-    if (c->halo_stream && overlap_on && m_loc0 >= 3 &&
+    if (hl.on) {
+        s->ktimer.begin(kFusedSpmv);
+        leaves[0] = spmv(0, 0, 0, nullptr);
+        s->ktimer.end(kFusedSpmv);
+    } else if (c->halo_stream && overlap_on && m_loc0 >= 3 &&
         spmv_plane_ranges<T>(view<T>(c, 0), c->fast())) {
         // ranks > 1: the ghost planes travel on the halo stream while the interior
         // planes (which never read a ghost) are swept; the two boundary planes follow

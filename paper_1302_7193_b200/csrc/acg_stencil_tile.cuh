@@ -293,7 +293,13 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     __syncthreads();
     pdl_wait();  // programmatic dependent launch: the previous grid has completed
     if (ld_dep(&S->done)) return;  // block-uniform
-    const int il = v.plane_begin + blockIdx.y;
+    int il = v.plane_begin + blockIdx.y;
+    if (v.halo.on) {  // fused halo: boundary planes last, after the neighbours' K1 put them
+        const int y = blockIdx.y, ml = v.m_loc;
+        if (ml >= 3) il = y < ml - 2 ? y + 1 : (y == ml - 2 ? 0 : ml - 1);
+        if (il == 0 && v.halo.ghost[0] != nullptr) halo_acquire(v.halo.wait_flag[0], v.halo.seq);
+        if (il == ml - 1 && v.halo.ghost[1] != nullptr) halo_acquire(v.halo.wait_flag[1], v.halo.seq);
+    }
     const int jr = blockIdx.x * 2 * NT + 2 * tid;
     const bool valid = jr < m;  // m even: both columns exist
     if (stage == nullptr && !valid) return;
@@ -312,7 +318,11 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     T* pc = p + base;
     T* qc = q + base;
     const long long sm = m;
-    const long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+    long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+    if (v.halo.on) {  // ghost rows straight from this rank's mailbox
+        if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
+        if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
+    }
     auto issue = [&](int k, int s) {
         const long long l = static_cast<long long>(k) * sm;
         P* r0 = ring + s * 7 * NT;

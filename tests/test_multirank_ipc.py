@@ -11,12 +11,21 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("world,port", [(2, 29611), (4, 29612)])
-def test_ipc_ranks_bit_exact(world, port):
+# halo variants: fused into the sweeps (K1 puts the boundary planes into the
+# neighbours' mailboxes, K2 acquires them; default), copy + signal on a side
+# stream overlapped with the interior sweep, and copy + signal in stream order
+HALO = {"fused": {}, "overlap": {"ACG_FUSED_HALO": "0"},
+        "serial": {"ACG_FUSED_HALO": "0", "ACG_HALO_OVERLAP": "0"}}
+
+
+@pytest.mark.parametrize("world,port,halo", [(2, 29611, "fused"), (4, 29612, "fused"),
+                                             (2, 29613, "overlap"), (4, 29614, "overlap"),
+                                             (2, 29615, "serial")])
+def test_ipc_ranks_bit_exact(world, port, halo):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(HERE, "mp_ipc_worker.py"), "64", "24"]
-    env = dict(os.environ, ACG_SAME_GPU="1", OMP_NUM_THREADS="1")
+    env = dict(os.environ, ACG_SAME_GPU="1", OMP_NUM_THREADS="1", **HALO[halo])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
