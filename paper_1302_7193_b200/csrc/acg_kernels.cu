@@ -766,6 +766,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
 // when the slabs are nodes of the reference tree, else the pairwise rule.
 template <typename T>
 __device__ T combine_slabs(const T* gather, int a, int nslabs, bool exact) {
+    if (nslabs == 1) return gather[a];
     T v[64];
     for (int s = 0; s < nslabs; ++s) v[s] = gather[s * 4 + a];
     if (exact) {
@@ -907,6 +908,90 @@ __global__ void __launch_bounds__(256)
         }
         __threadfence_system();
         for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+    }
+}
+
+// Stage 2, wide (nv <= 2): up to 1024 threads with C (<= 8) consecutive leaves each,
+// every array's leaves loaded up front with 16-byte loads, then the register
+// tree, a shuffle tree per warp and a shuffle tree over the (power-of-two many)
+// warps — the same perfect tree over nleaves = nthreads * C as k_tree2.
+template <typename T, int C>
+__global__ void __launch_bounds__(1024)
+    k_tree2_wide(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather,
+                 int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op,
+                 const IpcPut<T> put) {
+    pdl_trigger();  // the next sweep may start its prologue while this tree runs
+    pdl_wait();
+    if (op != kOpStore && S->done) {  // gated; the peer-memory put is unconditional
+        if (put.n > 0 && threadIdx.x == 0) {
+            __threadfence_system();
+            for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+        }
+        return;
+    }
+    __shared__ T wsum[2][32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int width = nt < 32 ? nt : 32;
+    T v[2][C];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        if (a < nv) {
+            const T* src = stage + a * static_cast<long long>(nleaves) + tid * C;
+            if constexpr (C % 2 == 0 && sizeof(T) == 8) {
+#pragma unroll
+                for (int l = 0; l < C; l += 2) {
+                    const double2 d = __ldcg(reinterpret_cast<const double2*>(src + l));
+                    v[a][l] = d.x;
+                    v[a][l + 1] = d.y;
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < C; ++l) v[a][l] = __ldcg(src + l);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        if (a < nv) {
+#pragma unroll
+            for (int w = 1; w < C; w <<= 1)
+#pragma unroll
+                for (int l = 0; l + w < C; l += 2 * w) v[a][l] = add_rn(v[a][l], v[a][l + w]);
+            T x = v[a][0];
+            for (int w = 1; w < width; w <<= 1) {
+                const T o = __shfl_down_sync(0xffffffffu >> (32 - width), x, w, width);
+                if ((lane & (2 * w - 1)) == 0) x = add_rn(x, o);
+            }
+            if (lane == 0) wsum[a][warp] = x;
+        }
+    }
+    const int nw = (nt + 31) / 32;  // a power of two
+    __syncthreads();
+    if (warp == 0) {
+        T sums[4] = {T(0), T(0), T(0), T(0)};
+        for (int a = 0; a < nv; ++a) {
+            T x = lane < nw ? wsum[a][lane] : T(0);
+            for (int w = 1; w < nw; w <<= 1) {
+                const T o = __shfl_down_sync(0xffffffffu, x, w);
+                if ((lane & (2 * w - 1)) == 0) x = add_rn(x, o);
+            }
+            if (lane == 0) gather[slab * 4 + a] = x;
+        }
+        if (lane == 0) {
+            if (finish) {
+                for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
+                run_op(S, op, sums);
+            }
+            if (put.n > 0) {  // rank `put.rank`'s 4 sums into every mailbox, then the flags
+                for (int q = 0; q < put.n; ++q) {
+                    T* d = put.dst[q] + put.rank * 4;
+                    for (int a = 0; a < 4; ++a) d[a] = gather[slab * 4 + a];
+                }
+                __threadfence_system();
+                for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+            }
+        }
     }
 }
 
@@ -1436,6 +1521,7 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             case 31: ACG_PR(false, 3, 1); break;
             case 33: ACG_PR(false, 3, 3); break;
             case 43: ACG_PR(false, 4, 3); break;
+            case -32: ACG_PR(true, 3, 2); break;
             default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
         }
 #undef ACG_PR
@@ -1600,6 +1686,23 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
         const char* e = std::getenv("ACG_TREE2");
         return e && std::string(e) == "legacy";
     }();
+    static const bool shfl = [] {
+        const char* e = std::getenv("ACG_TREE2");
+        return e && std::string(e) == "shfl";
+    }();
+    if (!legacy && !shfl && nv <= 2 && nl <= 1024 * 8) {
+        const int c = nl > 1024 ? nl / 1024 : 1;
+        const int nt = nl / c;
+        const int f = finish ? 1 : 0, ex = exact_tree ? 1 : 0;
+        switch (c) {
+            case 1: launch_pdl(k_tree2_wide<T, 1>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 2: launch_pdl(k_tree2_wide<T, 2>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            case 4: launch_pdl(k_tree2_wide<T, 4>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+            default: launch_pdl(k_tree2_wide<T, 8>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
+        }
+        post_launch("tree2");
+        return;
+    }
     if ((!legacy || pp.n > 0) && nl <= 256 * 64) {
         const int c = nl > 256 ? nl / 256 : 1;
         const int nt = nl / c;
