@@ -152,6 +152,11 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
                          const Scalars<T>* gate, T* phi_scratch, cudaStream_t st);
 // Can launch_fused_spmv sweep a sub-range of the slab's planes (halo overlap:
 // interior planes while the ghost planes are in flight, then the boundary)?
+// Most reduction-tree leaves a sweep's fused stage 1 may emit; slab.stage holds
+// 3 * max(k_tree1 blocks, kMaxFusedLeaves) values (stage 1.5 writes its nodes
+// after the leaves).
+constexpr int kMaxFusedLeaves = 131072;
+
 // true when the interleaved sweeps chosen for this view honour SlabView::halo
 // (K1 = k_thomas_tm default configuration, K2 = k_fused_spmv_pair2).
 template <typename T>

@@ -911,24 +911,14 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// Stage 2, wide (nv <= 2): up to 1024 threads with C (<= 8) consecutive leaves each,
-// every array's leaves loaded up front with 16-byte loads, then the register
-// tree, a shuffle tree per warp and a shuffle tree over the (power-of-two many)
-// warps — the same perfect tree over nleaves = nthreads * C as k_tree2.
+// Perfect tree over blockDim.x * C consecutive leaves of nv (<= 2) arrays
+// (array a at src + a * stride): C leaves per thread with 16-byte loads, the
+// register tree, a shuffle tree per warp and a shuffle tree over the
+// (power-of-two many) warps — the reference's pairwise tree restricted to an
+// aligned perfect subtree. Lane 0 of warp 0 returns the sums in out[].
 template <typename T, int C>
-__global__ void __launch_bounds__(1024)
-    k_tree2_wide(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather,
-                 int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op,
-                 const IpcPut<T> put) {
-    pdl_trigger();  // the next sweep may start its prologue while this tree runs
-    pdl_wait();
-    if (op != kOpStore && S->done) {  // gated; the peer-memory put is unconditional
-        if (put.n > 0 && threadIdx.x == 0) {
-            __threadfence_system();
-            for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
-        }
-        return;
-    }
+__device__ __forceinline__ void block_tree(const T* __restrict__ src, long long stride, int nv,
+                                           T (&out)[2]) {
     __shared__ T wsum[2][32];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -937,17 +927,17 @@ __global__ void __launch_bounds__(1024)
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
         if (a < nv) {
-            const T* src = stage + a * static_cast<long long>(nleaves) + tid * C;
+            const T* p = src + a * stride + tid * C;
             if constexpr (C % 2 == 0 && sizeof(T) == 8) {
 #pragma unroll
                 for (int l = 0; l < C; l += 2) {
-                    const double2 d = __ldcg(reinterpret_cast<const double2*>(src + l));
+                    const double2 d = __ldcg(reinterpret_cast<const double2*>(p + l));
                     v[a][l] = d.x;
                     v[a][l + 1] = d.y;
                 }
             } else {
 #pragma unroll
-                for (int l = 0; l < C; ++l) v[a][l] = __ldcg(src + l);
+                for (int l = 0; l < C; ++l) v[a][l] = __ldcg(p + l);
             }
         }
     }
@@ -969,28 +959,62 @@ __global__ void __launch_bounds__(1024)
     const int nw = (nt + 31) / 32;  // a power of two
     __syncthreads();
     if (warp == 0) {
-        T sums[4] = {T(0), T(0), T(0), T(0)};
         for (int a = 0; a < nv; ++a) {
             T x = lane < nw ? wsum[a][lane] : T(0);
             for (int w = 1; w < nw; w <<= 1) {
                 const T o = __shfl_down_sync(0xffffffffu, x, w);
                 if ((lane & (2 * w - 1)) == 0) x = add_rn(x, o);
             }
-            if (lane == 0) gather[slab * 4 + a] = x;
+            out[a] = x;
         }
-        if (lane == 0) {
-            if (finish) {
-                for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
-                run_op(S, op, sums);
+    }
+}
+
+// Stage 1.5 for more than 8192 leaves: CTA b reduces leaves [b * 8192, (b+1) * 8192)
+// (an aligned node of the tree) to mid[a * gridDim.x + b].
+template <typename T>
+__global__ void __launch_bounds__(1024)
+    k_tree_mid(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ mid) {
+    pdl_trigger();
+    pdl_wait();
+    T out[2];
+    block_tree<T, 8>(stage + static_cast<long long>(blockIdx.x) * 8192, nleaves, nv, out);
+    if (threadIdx.x == 0)
+        for (int a = 0; a < nv; ++a) mid[a * gridDim.x + blockIdx.x] = out[a];
+}
+
+// Stage 2, wide (nv <= 2): up to 1024 threads with C (<= 8) consecutive
+// leaves each (block_tree), then the finish / peer-memory put.
+template <typename T, int C>
+__global__ void __launch_bounds__(1024)
+    k_tree2_wide(int nleaves, const T* __restrict__ stage, int nv, T* __restrict__ gather,
+                 int slab, int finish, int nslabs, int exact, Scalars<T>* __restrict__ S, int op,
+                 const IpcPut<T> put) {
+    pdl_trigger();  // the next sweep may start its prologue while this tree runs
+    pdl_wait();
+    if (op != kOpStore && S->done) {  // gated; the peer-memory put is unconditional
+        if (put.n > 0 && threadIdx.x == 0) {
+            __threadfence_system();
+            for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+        }
+        return;
+    }
+    T out[2];
+    block_tree<T, C>(stage, nleaves, nv, out);
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < nv; ++a) gather[slab * 4 + a] = out[a];
+        if (finish) {
+            T sums[4] = {T(0), T(0), T(0), T(0)};
+            for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(gather, a, nslabs, exact != 0);
+            run_op(S, op, sums);
+        }
+        if (put.n > 0) {  // rank `put.rank`'s 4 sums into every mailbox, then the flags
+            for (int q = 0; q < put.n; ++q) {
+                T* d = put.dst[q] + put.rank * 4;
+                for (int a = 0; a < 4; ++a) d[a] = gather[slab * 4 + a];
             }
-            if (put.n > 0) {  // rank `put.rank`'s 4 sums into every mailbox, then the flags
-                for (int q = 0; q < put.n; ++q) {
-                    T* d = put.dst[q] + put.rank * 4;
-                    for (int a = 0; a < 4; ++a) d[a] = gather[slab * 4 + a];
-                }
-                __threadfence_system();
-                for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
-            }
+            __threadfence_system();
+            for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
         }
     }
 }
@@ -1125,7 +1149,8 @@ inline int thomas_choice() {
 
 // Leaves of the reduction tree a sweep can emit directly (cta_subtree_sums):
 // CTAs of `cols` consecutive columns of one i-plane, slab column count a power
-// of two (so every CTA is an aligned node), at most 16384 leaves (k_tree2).
+// of two (so every CTA is an aligned node), at most kMaxFusedLeaves leaves
+// (k_tree2_wide; above 8192 via the k_tree_mid nodes).
 // 0: the sweep writes per-column partials and k_tree1 runs instead.
 template <typename T>
 int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
@@ -1135,7 +1160,7 @@ int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
     }();
     if (off || stage == nullptr || cols <= 0 || v.m % cols != 0) return 0;
     const long long ncol = static_cast<long long>(v.m_loc) * v.m;
-    if ((ncol & (ncol - 1)) != 0 || ncol / cols > 16384 || ncol / cols < 1) return 0;
+    if ((ncol & (ncol - 1)) != 0 || ncol / cols > kMaxFusedLeaves || ncol / cols < 1) return 0;
     return static_cast<int>(ncol / cols);
 }
 
@@ -1690,6 +1715,17 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
         const char* e = std::getenv("ACG_TREE2");
         return e && std::string(e) == "shfl";
     }();
+    if (!legacy && !shfl && nv <= 2 && nl > 1024 * 8 && nl <= 1024 * 8 * 1024) {
+        // more leaves than one CTA takes: aligned nodes of 8192 leaves first
+        const int nb = nl / 8192;
+        T* mid = const_cast<T*>(stage) + static_cast<long long>(nv) * nl;
+        launch_pdl(k_tree_mid<T>, dim3(nb), dim3(1024), 0, st, nl, stage, nv, mid);
+        post_launch("tree_mid");
+        TreePlan p2 = plan;
+        p2.blocks = nb;
+        launch_tree_stage2<T>(p2, mid, nv, gather, slab, finish, nslabs, exact_tree, S, op, st, put);
+        return;
+    }
     if (!legacy && !shfl && nv <= 2 && nl <= 1024 * 8) {
         const int c = nl > 1024 ? nl / 1024 : 1;
         const int nt = nl / c;

@@ -595,8 +595,10 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
                      ncol);
             CK(cudaMalloc(&s.fin_counter, sizeof(int)));
             CK(cudaMemset(s.fin_counter, 0, sizeof(int)));
-            // stage: k_tree1 block sums, or up to 16384 node sums written by a sweep
-            CK(cudaMalloc(&s.stage, 3 * static_cast<size_t>(std::max(s.plan.blocks, 16384)) * c->s));
+            // stage: k_tree1 block sums, or up to kMaxFusedLeaves node sums written by a
+            // sweep followed by the stage-1.5 nodes
+            CK(cudaMalloc(&s.stage,
+                          3 * static_cast<size_t>(std::max(s.plan.blocks, kMaxFusedLeaves)) * c->s));
             if (thomas_smem_per_block(static_cast<int>(c->s), d->n_z, false) > 200 * 1024)
                 CK(cudaMalloc(&s.phi, s.n_loc * c->s));  // tall columns: phi in HBM
         }

@@ -5,7 +5,9 @@ The GPU solve of config 3 (fp64 1024^2 x 128, the headline workload), config 4
 field; skipped on hosts with < 128 GB RAM) is compared with the reference's
 own code compiled from source (oracle/_ref, OpenMP on all host cores) on the
 same inputs: identical residual/kappa/alpha/beta histories and solution, bit
-for bit. Plus size-independent properties of the full-size fields.
+for bit. Plus size-independent properties of the full-size fields. Two thin
+variants at configs 4/5's horizontal sizes exercise the multi-CTA reduction
+stage (more than 8192 tree leaves per sweep).
 """
 import os
 
@@ -20,6 +22,10 @@ CONFIGS = {
     "c3": dict(m=1024, n_z=128, dtype=np.float64, lambda2=3.32e-2, iters=3),
     "c4": dict(m=2048, n_z=128, dtype=np.float32, lambda2=1.0e2, iters=2),
     "c5": dict(m=4096, n_z=64, dtype=np.float64, lambda2=3.32e-2, iters=2),
+    # config 5's horizontal size with few levels: 131072 (K1) / 32768 (K2) reduction
+    # leaves from the sweeps, reduced through the k_tree_mid stage
+    "c5_thin": dict(m=4096, n_z=8, dtype=np.float64, lambda2=3.32e-2, iters=3),
+    "wide_2048": dict(m=2048, n_z=16, dtype=np.float64, lambda2=3.32e-2, iters=3),
 }
 
 
