@@ -50,11 +50,20 @@ def main():
         ug = np.concatenate([p_[1] for p_ in parts], axis=0)
         yg = np.concatenate([p_[2] for p_ in parts], axis=0)
         uo, ro = o.solve(o.random_field(42), epsilon=1e-9, maxiter=400)
-        ok = (info["exact_tree"] and res["iterations"] == ro.iterations
-              and np.array_equal(res["residual_history"], ro.residual_history)
-              and np.array_equal(res["kappa_history"], ro.kappa_history)
-              and np.array_equal(ug, uo) and np.array_equal(yg, o.apply(x))
-              and res["true_residual"] == ro.true_residual and tr == ro.true_residual)
+        if info["exact_tree"]:  # slabs are nodes of the reference's tree: bit for bit
+            ok = (res["iterations"] == ro.iterations
+                  and np.array_equal(res["residual_history"], ro.residual_history)
+                  and np.array_equal(res["kappa_history"], ro.kappa_history)
+                  and np.array_equal(ug, uo) and np.array_equal(yg, o.apply(x))
+                  and res["true_residual"] == ro.true_residual and tr == ro.true_residual)
+        else:  # slab sums combined pairwise: the north-star tolerances (fp64)
+            n = min(len(res["residual_history"]), len(ro.residual_history))
+            r0 = ro.residual_history[0]
+            ok = (abs(res["iterations"] - ro.iterations) <= 1
+                  and np.max(np.abs(np.asarray(res["residual_history"][:n])
+                                    - ro.residual_history[:n])) <= 1e-10 * r0
+                  and np.max(np.abs(ug - uo)) <= 1e-10 * np.max(np.abs(uo))
+                  and np.array_equal(yg, o.apply(x)))
         print(f"world={world} iterations={res['iterations']} (ref {ro.iterations}) "
               f"exact_tree={info['exact_tree']} {'IPC_OK' if ok else 'IPC_MISMATCH'}", flush=True)
     dist.barrier()

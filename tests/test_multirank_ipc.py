@@ -18,13 +18,17 @@ HALO = {"fused": {}, "overlap": {"ACG_FUSED_HALO": "0"},
         "serial": {"ACG_FUSED_HALO": "0", "ACG_HALO_OVERLAP": "0"}}
 
 
-@pytest.mark.parametrize("world,port,halo", [(2, 29611, "fused"), (4, 29612, "fused"),
-                                             (2, 29613, "overlap"), (4, 29614, "overlap"),
-                                             (2, 29615, "serial")])
-def test_ipc_ranks_bit_exact(world, port, halo):
+@pytest.mark.parametrize("world,port,halo,m", [(2, 29611, "fused", 64), (4, 29612, "fused", 64),
+                                               (2, 29613, "overlap", 64), (4, 29614, "overlap", 64),
+                                               (2, 29615, "serial", 64),
+                                               # two planes per rank; one plane per rank
+                                               # (4-column slabs are not tree nodes:
+                                               # compared within the fp64 tolerances)
+                                               (4, 29616, "fused", 8), (4, 29617, "fused", 4)])
+def test_ipc_ranks_bit_exact(world, port, halo, m):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(HERE, "mp_ipc_worker.py"), "64", "24"]
+           os.path.join(HERE, "mp_ipc_worker.py"), str(m), "24"]
     env = dict(os.environ, ACG_SAME_GPU="1", OMP_NUM_THREADS="1", **HALO[halo])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
