@@ -197,16 +197,22 @@ template <typename T>
 void launch_tree_stage1(const TreePlan& plan, const T* in0, const T* in1, const T* in2, int nv,
                         T* stage, const Scalars<T>* gate, cudaStream_t st);
 // Peer-memory ranks: stage 2 also copies the rank's 4 slab sums into every
-// rank's mailbox (dst[q] + rank*4) and releases flag[q][rank] = seq.
+// rank's mailbox (dst[q] + rank*4) and releases flag[q][rank] = seq. With
+// `wait` set, the same kernel then acquires wait[q] >= seq for every rank q,
+// combines all ranks' sums from its own mailbox (`all`) and runs the scalar
+// program — the whole cross-rank reduction in one launch.
 template <typename T>
 struct IpcPut {
     T* const* dst;
     unsigned long long* const* flag;
     int n, rank;
     unsigned long long seq;
+    const unsigned long long* wait = nullptr;
+    const T* all = nullptr;
 };
+// Returns true when the kernel also finished the reduction (IpcPut::wait).
 template <typename T>
-void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
+bool launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
                         bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
                         cudaStream_t st, const IpcPut<T>* put = nullptr);
 // wait_flags (peer-memory ranks): first wait until wait_flags[q] >= seq for all q < nslabs

@@ -911,6 +911,19 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Peer-memory ranks: acquire flags[q] >= seq for every rank q (traps after
+// ~20 s instead of hanging when a peer never arrives).
+__device__ __forceinline__ void ipc_wait_all(const unsigned long long* flags, int n,
+                                             unsigned long long seq) {
+    const long long t0 = clock64();
+    for (int q = 0; q < n; ++q)
+        while (ld_acquire_sys(flags + q) < seq) {
+            if (clock64() - t0 > (40ll << 30)) __trap();
+            __nanosleep(32);
+        }
+    __threadfence_system();
+}
+
 // Perfect tree over blockDim.x * C consecutive leaves of nv (<= 2) arrays
 // (array a at src + a * stride): C leaves per thread with 16-byte loads, the
 // register tree, a shuffle tree per warp and a shuffle tree over the
@@ -992,10 +1005,13 @@ __global__ void __launch_bounds__(1024)
                  const IpcPut<T> put) {
     pdl_trigger();  // the next sweep may start its prologue while this tree runs
     pdl_wait();
-    if (op != kOpStore && S->done) {  // gated; the peer-memory put is unconditional
+    if (op != kOpStore && S->done) {  // gated; the peer-memory flags stay in lockstep
         if (put.n > 0 && threadIdx.x == 0) {
             __threadfence_system();
             for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+            // still wait for every rank: no rank may run two reductions ahead and
+            // overwrite a mailbox parity a peer is still reading
+            if (put.wait != nullptr) ipc_wait_all(put.wait, put.n, put.seq);
         }
         return;
     }
@@ -1015,6 +1031,12 @@ __global__ void __launch_bounds__(1024)
             }
             __threadfence_system();
             for (int q = 0; q < put.n; ++q) st_release_sys(put.flag[q] + put.rank, put.seq);
+            if (put.wait != nullptr) {  // every rank's sums have landed: finish here
+                ipc_wait_all(put.wait, put.n, put.seq);
+                T sums[4] = {T(0), T(0), T(0), T(0)};
+                for (int a = 0; a < nv; ++a) sums[a] = combine_slabs(put.all, a, put.n, exact != 0);
+                run_op(S, op, sums);
+            }
         }
     }
 }
@@ -1702,10 +1724,10 @@ void launch_tree_stage1(const TreePlan& plan, const T* in0, const T* in1, const 
 }
 
 template <typename T>
-void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
+bool launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather, int slab,
                         bool finish, int nslabs, bool exact_tree, Scalars<T>* S, int op,
                         cudaStream_t st, const IpcPut<T>* put) {
-    const IpcPut<T> pp = put ? *put : IpcPut<T>{nullptr, nullptr, 0, 0, 0};
+    IpcPut<T> pp = put ? *put : IpcPut<T>{nullptr, nullptr, 0, 0, 0};
     const int nl = plan.blocks;  // power of two
     static const bool legacy = [] {
         const char* e = std::getenv("ACG_TREE2");
@@ -1723,8 +1745,8 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
         post_launch("tree_mid");
         TreePlan p2 = plan;
         p2.blocks = nb;
-        launch_tree_stage2<T>(p2, mid, nv, gather, slab, finish, nslabs, exact_tree, S, op, st, put);
-        return;
+        return launch_tree_stage2<T>(p2, mid, nv, gather, slab, finish, nslabs, exact_tree, S, op,
+                                     st, put);
     }
     if (!legacy && !shfl && nv <= 2 && nl <= 1024 * 8) {
         const int c = nl > 1024 ? nl / 1024 : 1;
@@ -1737,8 +1759,9 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
             default: launch_pdl(k_tree2_wide<T, 8>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
         }
         post_launch("tree2");
-        return;
+        return pp.wait != nullptr;
     }
+    pp.wait = nullptr;  // the other stage-2 kernels only put; k_finish waits and combines
     if ((!legacy || pp.n > 0) && nl <= 256 * 64) {
         const int c = nl > 256 ? nl / 256 : 1;
         const int nt = nl / c;
@@ -1753,12 +1776,13 @@ void launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
             default: launch_pdl(k_tree2_shfl<T, 64>, dim3(1), dim3(nt), 0, st, nl, stage, nv, gather, slab, f, nslabs, ex, S, op, pp); break;
         }
         post_launch("tree2");
-        return;
+        return false;
     }
     const int nt = nl < 1024 ? nl : 1024;
     k_tree2<T><<<1, nt, 0, st>>>(nl, stage, nv, gather, slab, finish ? 1 : 0, nslabs,
                                  exact_tree ? 1 : 0, S, op);
     post_launch("tree2");
+    return false;
 }
 
 template <typename T>
@@ -1817,7 +1841,7 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
     template void launch_fill_random<T>(const SlabView<T>&, uint64_t, T*, cudaStream_t);        \
     template void launch_tree_stage1<T>(const TreePlan&, const T*, const T*, const T*, int, T*, \
                                         const Scalars<T>*, cudaStream_t);                       \
-    template void launch_tree_stage2<T>(const TreePlan&, const T*, int, T*, int, bool, int,     \
+    template bool launch_tree_stage2<T>(const TreePlan&, const T*, int, T*, int, bool, int,     \
                                         bool, Scalars<T>*, int, cudaStream_t, const IpcPut<T>*); \
     template void launch_finish<T>(const T*, int, int, bool, Scalars<T>*, int, cudaStream_t,    \
                                    const unsigned long long*, unsigned long long);              \

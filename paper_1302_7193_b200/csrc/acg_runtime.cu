@@ -945,7 +945,16 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
         put.n = ip.p;
         put.rank = ip.rank;
         put.seq = seq;
+        static const bool fused_finish = [] {  // ACG_IPC_FINISH=kernel: separate k_finish (A/B)
+            const char* e = std::getenv("ACG_IPC_FINISH");
+            return !(e && std::string(e) == "kernel");
+        }();
+        if (fused_finish && c->slabs.size() == 1) {
+            put.wait = ip.flags(ip.rank) + 2;
+            put.all = reinterpret_cast<const T*>(ip.gather(ip.rank, par, c->s));
+        }
     }
+    bool finished = false;
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& s = c->slabs[si];
         const Scalars<T>* gate = gated ? (gate_or_null ? gate_or_null : S[si]) : nullptr;
@@ -960,11 +969,11 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
         }
         T* g = c->comm ? static_cast<T*>(c->gather_send) : gather;
         const int slot = c->comm ? 0 : s.index;
-        launch_tree_stage2<T>(plan, static_cast<const T*>(s.stage), nv, g, slot, single,
-                              c->nslabs_total, c->exact_tree, S[si], op, c->stream,
-                              put.n ? &put : nullptr);
+        finished = launch_tree_stage2<T>(plan, static_cast<const T*>(s.stage), nv, g, slot, single,
+                                         c->nslabs_total, c->exact_tree, S[si], op, c->stream,
+                                         put.n ? &put : nullptr);
     }
-    if (single) return;
+    if (single || finished) return;
     const unsigned long long* wait_flags = nullptr;
     if (c->ipc) {
         IpcState& ip = *c->ipc;
