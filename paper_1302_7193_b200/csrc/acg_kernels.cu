@@ -1347,13 +1347,19 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
                   Finish<T>* fin = nullptr) {
     const int tmc = thomas_tm_choice();
     const int tm2 = thomas_tm2_choice<T>();
-    if (v.halo.on) {  // fused halo (fused_halo_ok): the default TMEM sweep carries the planes
-        if (tmc == 0 || !v.tm_ok || phi_scratch != nullptr || thomas_tm_cols(v.n_z, sizeof(T)) > 256) {
-            std::fprintf(stderr, "acg: fused halo requested for a sweep that cannot carry it\n");
-            std::abort();
+    if (v.halo.on) {  // fused halo (fused_halo_ok): a TMEM sweep that carries the planes
+        if (tmc != 0 && v.tm_ok && phi_scratch == nullptr) {
+            if (tm2 != 0) {
+                const int l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Cfg<4, 15, 15>>(
+                    v, r, in, out, p2, pk, S, gate, stage, st);
+                if (l >= 0) return l;
+            }
+            if (thomas_tm_cols(v.n_z, sizeof(T)) <= 256)
+                return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmCfg<4, 15, 15>>(
+                    v, r, in, out, p2, pk, S, gate, stage, st, fin);
         }
-        return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmCfg<4, 15, 15>>(v, r, in, out, p2, pk, S,
-                                                                          gate, stage, st, fin);
+        std::fprintf(stderr, "acg: fused halo requested for a sweep that cannot carry it\n");
+        std::abort();
     }
     if (tm2 != 0 && tmc != 0 && v.tm_ok && phi_scratch == nullptr && !thomas_tma_enabled()) {
         int l = -1;
@@ -1475,8 +1481,13 @@ bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
         const char* e = std::getenv("ACG_FUSED_HALO");
         return e && std::string(e) == "0";
     }();
-    return !off && thomas_tm_choice() != 0 && v.tm_ok && !phi_in_hbm &&
-           thomas_tm_cols(v.n_z, sizeof(T)) <= 256 && spmv_mode<T>() == 6 && v.m % 2 == 0;
+    // producer: k_thomas_tm2 (fp32 default) or k_thomas_tm (default configuration);
+    // consumer: k_fused_spmv_pair (fp32 default) or k_fused_spmv_pair2 (fp64 default)
+    const unsigned cols = thomas_tm_cols(v.n_z, sizeof(T));
+    const bool k1 = (thomas_tm2_choice<T>() != 0 && 2 * cols <= 512) || cols <= 256;
+    const int mode = spmv_mode<T>();
+    return !off && thomas_tm_choice() != 0 && v.tm_ok && !phi_in_hbm && k1 &&
+           (mode == 5 || mode == 6) && v.m % 2 == 0;
 }
 
 template <typename T>
@@ -1493,7 +1504,7 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
     const dim3 block(32, kStencilWarps);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
     const int mode = spmv_mode<T>();
-    if (v.halo.on && !(mode == 6 && v.m % 2 == 0 && v.plane_count == 0)) {
+    if (v.halo.on && !((mode == 5 || mode == 6) && v.m % 2 == 0 && v.plane_count == 0)) {
         std::fprintf(stderr, "acg: fused halo requested for a stencil sweep that cannot carry it\n");
         std::abort();
     }

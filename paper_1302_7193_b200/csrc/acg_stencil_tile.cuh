@@ -179,7 +179,13 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     const int tid = threadIdx.y * 32 + threadIdx.x;
     load_profile(prof, v.prof, 4 * n_z, tid, NT);
     __syncthreads();
-    const int il = v.plane_begin + blockIdx.y;
+    int il = v.plane_begin + blockIdx.y;
+    if (v.halo.on) {  // fused halo: boundary planes last, after the neighbours' K1 put them
+        const int y = blockIdx.y, ml = v.m_loc;
+        if (ml >= 3) il = y < ml - 2 ? y + 1 : (y == ml - 2 ? 0 : ml - 1);
+        if (il == 0 && v.halo.ghost[0] != nullptr) halo_acquire(v.halo.wait_flag[0], v.halo.seq);
+        if (il == ml - 1 && v.halo.ghost[1] != nullptr) halo_acquire(v.halo.wait_flag[1], v.halo.seq);
+    }
     const int jr = blockIdx.x * 2 * NT + 2 * tid;
     const bool valid = jr < m;  // m even: both columns exist
     if (stage == nullptr && !valid) return;
@@ -214,8 +220,13 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
     T siga = T(0), sigb = T(0);
     // outside neighbours one level ahead: i+-1 rows as pairs, z(j-1), z(j+2)
-    const long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
-    P ze = *reinterpret_cast<const P*>(zc + oe), zw = *reinterpret_cast<const P*>(zc + ow);
+    long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+    if (v.halo.on) {  // ghost rows straight from this rank's mailbox
+        if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
+        if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
+    }
+    // i+-1 rows through L2 (coherent: the ghost rows may be a peer's fresh stores)
+    P ze = ldcg_pair<T>(zc + oe), zw = ldcg_pair<T>(zc + ow);
     T zs = zc[ca.os], zn = zc[1 + cb.on];
     int cs = 0, ps_ = D;
     for (int k = 0; k < n_z; ++k) {
@@ -224,8 +235,8 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         const T cs0 = zs, cn1 = zn;
         if (k + 1 < n_z) {
             const long long l1 = l + sm;
-            ze = *reinterpret_cast<const P*>(zc + l1 + oe);
-            zw = *reinterpret_cast<const P*>(zc + l1 + ow);
+            ze = ldcg_pair<T>(zc + l1 + oe);
+            zw = ldcg_pair<T>(zc + l1 + ow);
             zs = zc[l1 + ca.os];
             zn = zc[l1 + 1 + cb.on];
         }

@@ -37,6 +37,18 @@ __host__ __device__ constexpr size_t thomas_tm2_smem_bytes(int n_z) {
                         static_cast<size_t>(C::NS) * 2 * 2 * C::NT);
 }
 
+// 16- (fp64) or 8-byte (fp32) pair load through L2 (ld.global.cg).
+template <typename T>
+__device__ __forceinline__ Pair<T> ldcg_pair(const T* p) {
+    if constexpr (sizeof(T) == 8) {
+        const double2 d = __ldcg(reinterpret_cast<const double2*>(p));
+        return Pair<T>{d.x, d.y};
+    } else {
+        const float2 f = __ldcg(reinterpret_cast<const float2*>(p));
+        return Pair<T>{f.x, f.y};
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void cpa_pair(Pair<T>* sdst, const T* gsrc) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
@@ -245,7 +257,9 @@ __global__ void __launch_bounds__(C::NT, 1)
     const int top = n_z - 2;
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int il = tile / tiles_row;
+        int il = tile / tiles_row;
+        if (v.halo.on && il > 0)  // fused halo: the boundary planes first, their z travels
+            il = il == 1 ? v.m_loc - 1 : il - 1;
         const int j0 = (tile % tiles_row) * C::COLS;
         const int jr = j0 + 2 * tid;
         const bool valid = jr < m;  // m even: both columns of the pair exist
@@ -355,6 +369,37 @@ __global__ void __launch_bounds__(C::NT, 1)
             }
         }
         cp_wait<0>();
+        if (v.halo.on) {  // fused halo: z columns of a boundary plane -> neighbour's mailbox
+#pragma unroll
+            for (int sd = 0; sd < 2; ++sd) {
+                if (v.halo.put[sd] == nullptr || il != (sd == 0 ? 0 : v.m_loc - 1)) continue;
+                if (valid) {
+                    T* dst = v.halo.put[sd] + j;
+                    for (int k0 = 0; k0 < n_z; k0 += 8) {
+                        Pair<T> t8[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (k0 + u < n_z)
+                                t8[u] = ldcg_pair<T>(oc + static_cast<long long>(k0 + u) * sm);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (k0 + u < n_z)
+                                *reinterpret_cast<Pair<T>*>(dst + static_cast<long long>(k0 + u) * sm) =
+                                    t8[u];
+                    }
+                    __threadfence_system();
+                }
+                __syncthreads();  // tile-uniform branch
+                if (tid == 0) {
+                    __threadfence_system();
+                    if (atomicAdd(v.halo.arrive + sd, 1u) == static_cast<unsigned>(tiles_row) - 1) {
+                        atomicExch(v.halo.arrive + sd, 0u);
+                        __threadfence_system();
+                        st_release_sys(v.halo.put_flag[sd], v.halo.seq);
+                    }
+                }
+            }
+        }
         if (Fused && stage == nullptr && valid) {
             *reinterpret_cast<Pair<T>*>(part_r2 + cia) = Pair<T>{sa.r2, sb.r2};
             *reinterpret_cast<Pair<T>*>(part_k + cia) = Pair<T>{kapa, kapb};

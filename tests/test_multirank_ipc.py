@@ -24,11 +24,17 @@ HALO = {"fused": {}, "overlap": {"ACG_FUSED_HALO": "0"},
                                                # two planes per rank; one plane per rank
                                                # (4-column slabs are not tree nodes:
                                                # compared within the fp64 tolerances)
-                                               (4, 29616, "fused", 8), (4, 29617, "fused", 4)])
+                                               (4, 29616, "fused", 8), (4, 29617, "fused", 4),
+                                               # fp32: k_thomas_tm2 puts, k_fused_spmv_pair reads
+                                               (2, 29618, "fused-f32", 64),
+                                               (4, 29619, "fused-f32", 64),
+                                               (2, 29620, "overlap-f32", 64)])
 def test_ipc_ranks_bit_exact(world, port, halo, m):
+    f32 = halo.endswith("-f32")
+    halo = halo[:-4] if f32 else halo
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(HERE, "mp_ipc_worker.py"), str(m), "24"]
+           os.path.join(HERE, "mp_ipc_worker.py"), str(m), "24"] + (["f32"] if f32 else [])
     env = dict(os.environ, ACG_SAME_GPU="1", OMP_NUM_THREADS="1", **HALO[halo])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
