@@ -1174,6 +1174,16 @@ inline int thomas_choice() {
 // of two (so every CTA is an aligned node), at most kMaxFusedLeaves leaves
 // (k_tree2_wide; above 8192 via the k_tree_mid nodes).
 // 0: the sweep writes per-column partials and k_tree1 runs instead.
+inline int num_sms() {
+    static int n = [] {
+        int dev = 0, c = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+        return c;
+    }();
+    return n;
+}
+
 template <typename T>
 int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
     static const bool off = [] {
@@ -1196,7 +1206,22 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
     const dim3 block(32, C::W);
     constexpr int PW = C::W / C::X;  // i-planes per CTA
-    const dim3 grid((v.m + 32 * C::X - 1) / (32 * C::X), (v.m_loc + PW - 1) / PW);
+    // Planes per CTA (X = 4): one TMEM allocation and profile load serve tpc
+    // consecutive planes. Up to 4 while the grid keeps >= 6 waves of the 2
+    // resident CTAs per SM (C3: 4, K1 0.788 -> 0.776 ms; 8 per CTA: 0.855 ms,
+    // too few waves). ACG_TM_TPC=n overrides.
+    static const int tpc_env = [] {
+        const char* e = std::getenv("ACG_TM_TPC");
+        return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    int tpc = 1;
+    if (C::X == 4 && !v.halo.on && fin == nullptr) {
+        const long long ctas = static_cast<long long>((v.m + 127) / 128) * v.m_loc;
+        tpc = tpc_env ? tpc_env
+                      : static_cast<int>(std::min(4LL, std::max(1LL, ctas / (6LL * 2 * num_sms()))));
+    }
+    const dim3 grid((v.m + 32 * C::X - 1) / (32 * C::X),
+                    C::X == 4 ? (v.m_loc + tpc - 1) / tpc : (v.m_loc + PW - 1) / PW);
     size_t smem = thomas_tm_smem_bytes<T, C>(v.n_z);
     static const size_t occ_cap = [] {  // ACG_TM_OCC=n caps resident CTAs per SM (experiments)
         const char* e = std::getenv("ACG_TM_OCC");
@@ -1217,7 +1242,8 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     }
     ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
     launch_pdl(k_thomas_tm<T, Fast, Fused, C>, grid, block, smem, st, v, r, in, out, p2, pk,
-               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, fd);
+               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, fd,
+               tpc);
     return leaves;
 }
 
@@ -1275,15 +1301,6 @@ int launch_thomas_tma_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
     return leaves;
 }
 
-inline int num_sms() {
-    static int n = [] {
-        int dev = 0, c = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
-        return c;
-    }();
-    return n;
-}
 
 // Two columns per thread, persistent (k_thomas_tm2); -1 if not applicable.
 template <typename T, bool Fast, bool Fused, class C>
