@@ -80,12 +80,14 @@ acg_status acg_host_free(void* ptr);
 acg_status acg_comm_unique_id(void* id128);
 acg_status acg_comm_create(acg_comm** out, int rank, int nranks, const void* id128, int device);
 /* Peer-memory communicator for the ranks of ONE node (no NCCL): halo planes
- * and reduction slab sums are copied straight into the neighbours' / peers'
+ * and reduction slab sums are written straight into the neighbours' / peers'
  * device mailboxes through CUDA IPC mappings (NVLink P2P between GPUs; ranks
- * may also share a GPU), completion signalled by release/acquire flags in peer
- * memory. `id128`: identical on all ranks, unique per communicator (e.g. 16+
- * random bytes broadcast by rank 0); contexts must be created in the same order
- * on every rank (their mailboxes rendezvous under /dev/shm). */
+ * may also share a GPU) — in the interleaved loop by the sweep and reduction
+ * kernels themselves — with completion signalled by release/acquire flags in
+ * peer memory. `id128`: identical on all ranks, unique per communicator (16
+ * random bytes broadcast by rank 0 are enough; the first 16 are used);
+ * contexts must be created in the same order on every rank (their mailboxes
+ * rendezvous under /dev/shm). */
 acg_status acg_comm_create_ipc(acg_comm** out, int rank, int nranks, const void* id128,
                                int device);
 acg_status acg_comm_destroy(acg_comm* comm);
