@@ -248,7 +248,7 @@ def run_gpu(args, cfg):
     f = ctx.field().fill_random(42)
     variant = capi.INTERLEAVED if args.variant == "interleaved" else capi.STANDARD
     solver = capi.Solver(ctx, epsilon=1e-300, tau=1e-300,
-                         maxiter=args.warmup + 2 * args.steps + 8, variant=variant)
+                         maxiter=args.warmup + 3 * args.steps + 8, variant=variant)
     solver.start(f)
     solver.iterate(args.warmup)
     ctx.sync()
@@ -258,16 +258,32 @@ def run_gpu(args, cfg):
     # per-launch K1/K2 events cost ~1% of the step (they sit between the PDL
     # launches), so the headline pass runs without them and a second pass of
     # the same K steps times every K1/K2 launch for the roofline
-    solver.time_kernels(args.ktime_inline)
-    launches_before = capi.launch_count()
-    with ClockSampler(dev) as clk:
-        ev0.record(stream)
-        solver.iterate(args.steps)
-        ev1.record(stream)
-        ev1.synchronize()
-    barrier()
-    launches_timed = capi.launch_count() - launches_before
-    ms = ev0.elapsed_time(ev1)
+    def timed_pass():
+        solver.time_kernels(args.ktime_inline)
+        launches_before = capi.launch_count()
+        with ClockSampler(dev) as clk:
+            ev0.record(stream)
+            solver.iterate(args.steps)
+            ev1.record(stream)
+            ev1.synchronize()
+        barrier()
+        return ev0.elapsed_time(ev1), capi.launch_count() - launches_before, clk
+
+    ms, launches_timed, clk = timed_pass()
+    # a pass that saw a hardware / thermal slowdown is rejected and re-measured
+    # once (sw_power_cap is the board's normal steady state and is kept)
+    bad = bool({"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+               & set(clk.summary()["reasons"]))
+    if world > 1:
+        import torch.distributed as dist
+        fl = torch.tensor([1.0 if bad else 0.0], device=pg_dev)
+        dist.all_reduce(fl, op=dist.ReduceOp.MAX)
+        bad = fl.item() > 0
+    remeasured = False
+    if bad:
+        time.sleep(2.0)
+        ms, launches_timed, clk = timed_pass()
+        remeasured = True
     if not args.ktime_inline and not args.no_ktime:
         solver.time_kernels(True)
         solver.iterate(args.steps)
@@ -388,7 +404,7 @@ def run_gpu(args, cfg):
             "achieved_gbs_iteration": iter_gbs, "algorithmic_bytes_iteration": iter_bytes,
             "frac_of_peak_iteration": iter_gbs / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches_timed, "clocks": clk.summary(),
+            "gpu_launches": launches_timed, "clocks": dict(clk.summary(), remeasured=remeasured),
             "exact_tree": bool(info["exact_tree"]),
             "residual_after": float(res["residual_history"][-1]) if res["residual_history"].size else None,
         }
