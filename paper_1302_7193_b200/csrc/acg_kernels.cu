@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -1207,18 +1208,29 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     const dim3 block(32, C::W);
     constexpr int PW = C::W / C::X;  // i-planes per CTA
     // Planes per CTA (X = 4): one TMEM allocation and profile load serve tpc
-    // consecutive planes. Up to 4 while the grid keeps >= 6 waves of the 2
-    // resident CTAs per SM (C3: 4, K1 0.788 -> 0.776 ms; 8 per CTA: 0.855 ms,
-    // too few waves). ACG_TM_TPC=n overrides.
+    // consecutive planes. The largest tpc <= 4 that keeps >= 6 waves of the 2
+    // resident CTAs per SM with a last wave >= 97% full (C3: 4, K1 0.789 ->
+    // 0.777 ms; tpc 3, 5, 6 leave a 24-62% last wave: 0.80-0.81 ms; 8: 0.855 ms).
+    // ACG_TM_TPC=n overrides.
     static const int tpc_env = [] {
         const char* e = std::getenv("ACG_TM_TPC");
         return e ? std::max(1, std::atoi(e)) : 0;
     }();
     int tpc = 1;
     if (C::X == 4 && !v.halo.on && fin == nullptr) {
-        const long long ctas = static_cast<long long>((v.m + 127) / 128) * v.m_loc;
-        tpc = tpc_env ? tpc_env
-                      : static_cast<int>(std::min(4LL, std::max(1LL, ctas / (6LL * 2 * num_sms()))));
+        if (tpc_env) {
+            tpc = tpc_env;
+        } else {
+            const double slots = 2.0 * num_sms();
+            const long long rows = (v.m + 127) / 128;
+            for (int t = 4; t > 1; --t) {
+                const double waves = static_cast<double>(rows * ((v.m_loc + t - 1) / t)) / slots;
+                if (waves >= 6.0 && waves / std::ceil(waves) >= 0.97) {
+                    tpc = t;
+                    break;
+                }
+            }
+        }
     }
     const dim3 grid((v.m + 32 * C::X - 1) / (32 * C::X),
                     C::X == 4 ? (v.m_loc + tpc - 1) / tpc : (v.m_loc + PW - 1) / PW);
