@@ -220,20 +220,53 @@ def run_gpu(args, cfg):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        if args.transport == "nccl":
-            obj = [capi.Comm.unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            comm = capi.Comm(rank, world, obj[0], dev)
-        else:  # peer memory (CUDA IPC mailboxes over NVLink P2P), no NCCL on the data path
-            obj = [os.urandom(16) if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            comm = capi.Comm.ipc(rank, world, obj[0], dev)
     dtype = capi.F32 if cfg["dtype"] == "f32" else capi.F64
     s = 4 if dtype == capi.F32 else 8
     math_mode = capi.FAST if args.math == "fast" else capi.EXACT
     profile, panel = setup_arrays(cfg)
-    ctx = capi.Context.from_setup(profile, panel, dtype=dtype, math=math_mode, device=dev,
-                                  comm=comm, slabs=1 if comm else args.slabs)
+
+    def make_comm(transport):
+        import torch.distributed as dist
+        if transport == "nccl":
+            obj = [capi.Comm.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            return capi.Comm(rank, world, obj[0], dev)
+        # peer memory (CUDA IPC mailboxes over NVLink P2P), no NCCL on the data path
+        obj = [os.urandom(16) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return capi.Comm.ipc(rank, world, obj[0], dev)
+
+    def make_ctx(c):
+        return capi.Context.from_setup(profile, panel, dtype=dtype, math=math_mode, device=dev,
+                                       comm=c, slabs=1 if c else args.slabs)
+
+    if world > 1:
+        import torch.distributed as dist
+        ctx = None
+        try:
+            comm = make_comm(args.transport)
+            ctx = make_ctx(comm)
+            ok = 1.0
+        except Exception as exc:  # e.g. no CUDA IPC between the rank processes
+            print(f"bench: {args.transport} transport unavailable on rank {rank}: {exc}",
+                  file=sys.stderr)
+            ok = 0.0
+        fl = torch.tensor([ok], device=pg_dev)
+        dist.all_reduce(fl, op=dist.ReduceOp.MIN)
+        if fl.item() < 1.0 and args.transport != "nccl":
+            for h in (ctx, comm):
+                try:
+                    if h is not None:
+                        h.close()
+                except Exception:
+                    pass
+            args.transport = "nccl (peer-memory transport unavailable)"
+            comm = make_comm("nccl")
+            ctx = make_ctx(comm)
+        elif fl.item() < 1.0:
+            raise SystemExit("bench: no multi-GPU transport")
+    else:
+        ctx = make_ctx(None)
     info = ctx.info()
     stream = torch.cuda.ExternalStream(ctx.stream)
     launches0 = capi.launch_count()
