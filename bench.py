@@ -158,8 +158,7 @@ def run_reference_impl(args, cfg):
         from oracle.oracle import ref_available
         if not ref_available():
             raise RuntimeError("oracle/_ref not built")
-        for _ in range(max(args.warmup, 0)):
-            pass  # the 1-iteration warm-up solve below is the reference's own protocol
+        # cpu_reference runs the reference's own warm-up solve before the timed one
         r = cpu_reference(cfg, args.steps, cores)
         kind = "reference"
     except Exception as exc:  # the C port is the fallback checker
