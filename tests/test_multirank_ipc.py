@@ -15,7 +15,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # neighbours' mailboxes, K2 acquires them; default), copy + signal on a side
 # stream overlapped with the interior sweep, and copy + signal in stream order
 HALO = {"fused": {}, "overlap": {"ACG_FUSED_HALO": "0"},
-        "serial": {"ACG_FUSED_HALO": "0", "ACG_HALO_OVERLAP": "0"}}
+        "serial": {"ACG_FUSED_HALO": "0", "ACG_HALO_OVERLAP": "0"},
+        # reduction finished by a separate k_finish instead of inside stage 2
+        "kfinish": {"ACG_IPC_FINISH": "kernel"}}
 
 
 @pytest.mark.parametrize("world,port,halo,m", [(2, 29611, "fused", 64), (4, 29612, "fused", 64),
@@ -28,7 +30,8 @@ HALO = {"fused": {}, "overlap": {"ACG_FUSED_HALO": "0"},
                                                # fp32: k_thomas_tm2 puts, k_fused_spmv_pair reads
                                                (2, 29618, "fused-f32", 64),
                                                (4, 29619, "fused-f32", 64),
-                                               (2, 29620, "overlap-f32", 64)])
+                                               (2, 29620, "overlap-f32", 64),
+                                               (4, 29621, "kfinish", 64)])
 def test_ipc_ranks_bit_exact(world, port, halo, m):
     f32 = halo.endswith("-f32")
     halo = halo[:-4] if f32 else halo
