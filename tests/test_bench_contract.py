@@ -1,0 +1,44 @@
+"""bench.py's reference arm keeps the driver's JSON contract (CPU only).
+
+`bench.py --impl reference` times the reference's own CPU implementation
+(oracle/_ref, else the C port) and prints one JSON line with the contract's
+keys; under torchrun only rank 0 prints, the other ranks exit 0 without work.
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(extra_env=None):
+    env = dict(os.environ, OMP_NUM_THREADS="2", **(extra_env or {}))
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                           "--config", "c1", "--steps", "2", "--warmup", "1"],
+                          capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+
+
+def test_reference_arm_json_line():
+    r = run()
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["unit"] == "iter/s" and d["value"] > 0
+    assert d["higher_is_better"] is True and d["steps"] == 2
+    cb = d["cpu_baseline"]
+    assert cb["value"] == d["value"] and cb["cores"] >= 1 and cb["kind"] and cb["sample"]
+    e = d["e2e"]
+    assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 == e["d2h_bytes_per_step"]
+    assert d["config"]["workload"] and "model" not in d["config"]
+
+
+def test_reference_arm_other_ranks_silent():
+    r = run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip() == ""
