@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ACG_ABI_VERSION 1
+#define ACG_ABI_VERSION 2
 
 typedef enum {
     ACG_OK = 0,
@@ -218,12 +218,23 @@ typedef struct {
     int n_residual, n_kappa, n_alpha, n_beta; /* history lengths written */
     acg_kernel_timings timings;
     long long kernel_launches; /* device kernels launched by this solve */
+    /* Library-allocated copies of the residual, kappa, alpha and beta histories
+     * (n_residual, n_kappa, n_alpha, n_beta entries), filled for every history
+     * whose caller buffer is NULL; free them with acg_solve_result_release.
+     * This is how a caller with an "unbounded" maxiter (the reference only
+     * pushes what runs, solver.hpp:196-364) gets histories without
+     * pre-allocating maxiter+2 entries. */
+    double* history[4];
 } acg_solve_result;
 
 void acg_solver_config_default(acg_solver_config* cfg);
+/* Frees res->history[*] (safe on a zeroed or already released result). */
+void acg_solve_result_release(acg_solve_result* res);
 
 /* solve(), solver.hpp:373-378. Device fields; u0 may be NULL (zero start).
- * History buffers (capacity maxiter+2 doubles each) may be NULL. */
+ * History buffers, when not NULL, need room for maxiter+2 doubles each; pass
+ * NULL to receive library-allocated copies in res->history instead.
+ * Concurrent calls on one context are safe: they serialise on the context. */
 acg_status acg_solve(const acg_context* ctx, const acg_field* f, const acg_field* u0,
                      const acg_solver_config* cfg, acg_field* u_out, acg_solve_result* res,
                      double* residual_history, double* kappa_history, double* alpha_history,
@@ -241,6 +252,16 @@ acg_status acg_solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* 
                              double* alpha_history, double* beta_history);
 /* CUDA stream (cudaStream_t) the context's first local slab runs on. */
 void* acg_context_stream(const acg_context* ctx);
+/* Stream ordering with a caller's stream (cudaStream_t; NULL = the legacy
+ * default stream), e.g. torch.cuda.current_stream(): the context's stream
+ * waits for the work enqueued on `stream` so far (before reading a caller's
+ * device buffer), or `stream` waits for the context's work (before the caller
+ * consumes a result). Host-side non-blocking. */
+acg_status acg_context_wait_stream(const acg_context* ctx, void* stream);
+acg_status acg_stream_wait_context(void* stream, const acg_context* ctx);
+/* Frees the context's cached scratch (solver work fields, scratch-field
+ * pool, host-transfer staging); they are re-created on demand. */
+acg_status acg_context_release_scratch(const acg_context* ctx);
 /* Per-launch device time of the fused sweeps enqueued since the last call (ms,
  * CUDA events on the launching stream): returns counts and summed times. */
 acg_status acg_solver_kernel_times(acg_solver* s, int* n_prec, double* ms_prec, int* n_spmv,

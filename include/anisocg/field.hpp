@@ -96,6 +96,8 @@ inline acg_layout layout_of(Layout l) {
 
 /// Device context for context-free field operations (zero operator; shape only).
 acg_context* shape_context(acg_dtype dtype, int m, int n_z);
+/// Frees a context's pooled scratch fields, cached solver state and staging.
+void release_scratch(const acg_context* c);
 
 /// Scratch device field of a context, returned to a per-context pool on release.
 struct Scratch {
@@ -117,6 +119,11 @@ void download(const acg_field* f, Field3D<T>& x) {
 }
 
 }  // namespace detail
+
+/// Frees the device scratch the host API keeps between calls (pooled
+/// fields, staging buffers, cached solver state of the shape-only contexts);
+/// it is re-created on demand.
+void release_device_scratch();
 
 /// field.hpp:102-109 — value-preserving permutation (pure data movement).
 template <typename T>

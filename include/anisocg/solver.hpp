@@ -86,20 +86,21 @@ std::pair<Field3D<T>, SolveResult> run_solve(const OperatorContext<T>& ctx, cons
     c.workers = cfg.workers;
     c.variant = variant == Variant::interleaved ? ACG_VARIANT_INTERLEAVED : ACG_VARIANT_STANDARD;
     c.record_timings = 1;
-    const std::size_t cap = static_cast<std::size_t>(cfg.maxiter) + 2;
-    std::vector<double> hr(cap), hk(cap), ha(cap), hb(cap);
     Field3D<T> u(f.m(), f.n_z(), f.layout());
     acg_solve_result r{};
+    // NULL history buffers: the library returns exactly the pushed entries
+    // (no maxiter-sized allocation, like the reference's push_back histories)
     check(acg_solve_host(ctx.device(), layout_of(f.layout()), f.data(), u0.data(), &c, u.data(),
-                         &r, hr.data(), hk.data(), ha.data(), hb.data()));
+                         &r, nullptr, nullptr, nullptr, nullptr));
     SolveResult res;
     res.iterations = r.iterations;
     res.converged = r.converged != 0;
     res.true_residual = r.true_residual;
-    res.residual_history.assign(hr.begin(), hr.begin() + r.n_residual);
-    res.kappa_history.assign(hk.begin(), hk.begin() + r.n_kappa);
-    res.alpha_history.assign(ha.begin(), ha.begin() + r.n_alpha);
-    res.beta_history.assign(hb.begin(), hb.begin() + r.n_beta);
+    res.residual_history.assign(r.history[0], r.history[0] + r.n_residual);
+    res.kappa_history.assign(r.history[1], r.history[1] + r.n_kappa);
+    res.alpha_history.assign(r.history[2], r.history[2] + r.n_alpha);
+    res.beta_history.assign(r.history[3], r.history[3] + r.n_beta);
+    acg_solve_result_release(&r);
     res.timings.spmv = r.timings.spmv;
     res.timings.prec = r.timings.prec;
     res.timings.blas = r.timings.blas;

@@ -34,6 +34,7 @@ try:
         planar_panel,
         precondition,
         random_field,
+        release_scratch,
         scal,
         solve,
         true_residual,
@@ -80,5 +81,5 @@ __all__ = [
     "VerticalGrid", "VerticalProfile", "anisotropy", "apply", "assemble_csr", "axpy",
     "cost_model", "cubed_sphere_panel", "dot", "interleaved_prec_kernel",
     "interleaved_spmv_kernel", "kernel_launch_count", "nrm2", "planar_panel", "precondition",
-    "random_field", "scal", "solve", "true_residual", "vertical_grid", "vertical_profile",
+    "random_field", "release_scratch", "scal", "solve", "true_residual", "vertical_grid", "vertical_profile",
 ]

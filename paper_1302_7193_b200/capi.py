@@ -63,7 +63,8 @@ class KernelTimings(C.Structure):
 class SolveResult(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("true_residual", C.c_double),
                 ("n_residual", C.c_int), ("n_kappa", C.c_int), ("n_alpha", C.c_int),
-                ("n_beta", C.c_int), ("timings", KernelTimings), ("kernel_launches", C.c_longlong)]
+                ("n_beta", C.c_int), ("timings", KernelTimings), ("kernel_launches", C.c_longlong),
+                ("history", C.POINTER(C.c_double) * 4)]
 
 
 _lib = None
@@ -114,6 +115,10 @@ def lib():
         "acg_interleaved_spmv_kernel": (ip, [vp, vp, vp, vp, vp, C.c_double, C.c_double, dp]),
         "acg_interleaved_prec_kernel": (ip, [vp, vp, vp, vp, C.c_double, dp, dp]),
         "acg_solver_config_default": (None, [C.POINTER(SolverConfig)]),
+        "acg_solve_result_release": (None, [C.POINTER(SolveResult)]),
+        "acg_context_wait_stream": (ip, [vp, vp]),
+        "acg_stream_wait_context": (ip, [vp, vp]),
+        "acg_context_release_scratch": (ip, [vp]),
         "acg_solve": (ip, [vp, vp, vp, C.POINTER(SolverConfig), vp, C.POINTER(SolveResult),
                            vp, vp, vp, vp]),
         "acg_solver_create": (ip, [pp, vp, C.POINTER(SolverConfig)]),
@@ -253,6 +258,18 @@ class Context:
     def stream(self):
         return lib().acg_context_stream(self.h)
 
+    def wait_for(self, stream):
+        """The context's stream waits for the work enqueued on `stream` so far."""
+        check(lib().acg_context_wait_stream(self.h, C.c_void_p(stream or None)))
+
+    def signal_to(self, stream):
+        """`stream` waits for the work enqueued on the context's stream so far."""
+        check(lib().acg_stream_wait_context(C.c_void_p(stream or None), self.h))
+
+    def release_scratch(self):
+        """Free cached scratch (solver work fields, pooled fields, staging)."""
+        check(lib().acg_context_release_scratch(self.h))
+
     def field(self):
         return Field(self)
 
@@ -274,6 +291,21 @@ class Context:
 def is_cuda_array(a):
     """True for device arrays exposing __cuda_array_interface__ (torch, CuPy)."""
     return hasattr(a, "__cuda_array_interface__")
+
+
+def array_stream(a):
+    """cudaStream_t handle of the stream that produces / consumes a CUDA array:
+    torch's current stream for torch tensors, else the __cuda_array_interface__
+    v3 'stream' key (1 = legacy default, 2 = per-thread default; absent/None:
+    the legacy default stream)."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            return torch.cuda.current_stream(a.device).cuda_stream
+    except ImportError:  # pragma: no cover - torch is part of this image
+        pass
+    st = a.__cuda_array_interface__.get("stream")
+    return int(st) if st else 0
 
 
 def cuda_array_ptr(a, dtype, shape):
@@ -316,8 +348,10 @@ class Field:
         anything with __cuda_array_interface__) on the context's device."""
         if is_cuda_array(a):
             ptr = cuda_array_ptr(a, self.ctx.np_dtype, self._shape(layout, scope))
+            st = array_stream(a)
+            self.ctx.wait_for(st)    # the producer's pending writes land first
             check(lib().acg_field_upload_device(self.h, C.c_void_p(ptr), layout, scope))
-            self.ctx.sync()  # the source buffer belongs to another stream's owner
+            self.ctx.signal_to(st)   # later work on the owner's stream (frees, reuse) waits for the read
             return self
         a = np.ascontiguousarray(a, dtype=self.ctx.np_dtype)
         check(lib().acg_field_upload(self.h, _vptr(a), layout, scope))
@@ -327,8 +361,10 @@ class Field:
         """To a host array, or (out = a CUDA array) device to device."""
         if out is not None and is_cuda_array(out):
             ptr = cuda_array_ptr(out, self.ctx.np_dtype, self._shape(layout, scope))
+            st = array_stream(out)
+            self.ctx.wait_for(st)    # pending work on the output's memory finishes first
             check(lib().acg_field_download_device(self.h, C.c_void_p(ptr), layout, scope))
-            self.ctx.sync()
+            self.ctx.signal_to(st)   # the consumer's stream sees the result
             return out
         if out is None:
             out = np.empty(self._shape(layout, scope), dtype=self.ctx.np_dtype)
@@ -413,13 +449,20 @@ def config(epsilon=1e-5, tau=1e-20, maxiter=500, variant=INTERLEAVED, timings=Fa
     return c
 
 
-def _result(res, hs):
+def _result(res):
+    """SolveResult dict from an acg_solve_result whose histories the library
+    allocated (NULL caller buffers); releases them."""
     t = res.timings
+    try:
+        hs = [np.ctypeslib.as_array(res.history[a], shape=(n,)).copy() if n > 0 else np.zeros(0)
+              for a, n in enumerate((res.n_residual, res.n_kappa, res.n_alpha, res.n_beta))]
+    finally:
+        lib().acg_solve_result_release(C.byref(res))
     return {
         "iterations": res.iterations, "converged": bool(res.converged),
         "true_residual": res.true_residual,
-        "residual_history": hs[0][:res.n_residual].copy(), "kappa_history": hs[1][:res.n_kappa].copy(),
-        "alpha_history": hs[2][:res.n_alpha].copy(), "beta_history": hs[3][:res.n_beta].copy(),
+        "residual_history": hs[0], "kappa_history": hs[1],
+        "alpha_history": hs[2], "beta_history": hs[3],
         "timings": {k: getattr(t, k) for k, _ in KernelTimings._fields_},
         "kernel_launches": res.kernel_launches,
     }
@@ -427,11 +470,10 @@ def _result(res, hs):
 
 def solve(ctx, f: Field, u0: Field | None = None, u_out: Field | None = None, **kw):
     cfg = config(**kw)
-    hs = [np.zeros(cfg.maxiter + 2) for _ in range(4)]
     res = SolveResult()
     check(lib().acg_solve(ctx.h, f.h, u0.h if u0 else None, C.byref(cfg), u_out.h if u_out else None,
-                          C.byref(res), *[_vptr(h) for h in hs]))
-    return _result(res, hs)
+                          C.byref(res), None, None, None, None))
+    return _result(res)
 
 
 def solve_host(ctx, f, u0=None, layout=VERTICAL, out=None, **kw):
@@ -439,12 +481,11 @@ def solve_host(ctx, f, u0=None, layout=VERTICAL, out=None, **kw):
     cfg = config(**kw)
     f = np.ascontiguousarray(f, dtype=ctx.np_dtype)
     u = out if out is not None else np.empty_like(f)
-    hs = [np.zeros(cfg.maxiter + 2) for _ in range(4)]
     res = SolveResult()
     check(lib().acg_solve_host(ctx.h, layout, _vptr(f),
                                _vptr(np.ascontiguousarray(u0, dtype=ctx.np_dtype)) if u0 is not None else None,
-                               C.byref(cfg), _vptr(u), C.byref(res), *[_vptr(h) for h in hs]))
-    return u, _result(res, hs)
+                               C.byref(cfg), _vptr(u), C.byref(res), None, None, None, None))
+    return u, _result(res)
 
 
 class Solver:
@@ -473,11 +514,10 @@ class Solver:
         return {"fused_prec": (n1.value, t1.value), "fused_spmv": (n2.value, t2.value)}
 
     def finish(self, u_out=None):
-        hs = [np.zeros(self.cfg.maxiter + 2) for _ in range(4)]
         res = SolveResult()
         check(lib().acg_solver_finish(self.h, u_out.h if u_out else None, C.byref(res),
-                                      *[_vptr(h) for h in hs]))
-        return _result(res, hs)
+                                      None, None, None, None))
+        return _result(res)
 
     def close(self):
         if self.h:

@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cstddef>
 #include <cstdint>
 
@@ -87,7 +89,7 @@ struct Scalars {
     int done, converged, error;
     int n_res, n_kap, n_alp, n_bet;
     int pivot;  // written by the Thomas kernels on a zero pivot
-    int pad_;
+    int hmask;  // history arrays are rings of hmask + 1 entries (the host drains them)
     double* h_res;
     double* h_kap;
     double* h_alp;
@@ -134,7 +136,7 @@ struct Finish {
 };
 
 // ----------------------------------------------------------------- launchers
-extern long long g_launches;  // kernel launches issued (all entry points)
+extern std::atomic<long long> g_launches;  // kernel launches issued (all entry points)
 
 // The fused sweeps return the number of reduction-tree leaves they wrote to
 // `stage` (cta_subtree_sums; stage == nullptr or 0: per-column partials were
@@ -156,6 +158,9 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
 // 3 * max(k_tree1 blocks, kMaxFusedLeaves) values (stage 1.5 writes its nodes
 // after the leaves).
 constexpr int kMaxFusedLeaves = 131072;
+// Entries per device history ring (Scalars::hmask + 1); the solver loop drains
+// them to host vectors, so histories of any length fit (maxiter = 1e9 works).
+constexpr int kHistRing = 4096;
 
 // true when the interleaved sweeps chosen for this view honour SlabView::halo
 // (K1 = k_thomas_tm default configuration, K2 = k_fused_spmv_pair2).

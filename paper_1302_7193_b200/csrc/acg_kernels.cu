@@ -33,7 +33,7 @@
 
 namespace acg {
 
-long long g_launches = 0;
+std::atomic<long long> g_launches{0};
 
 namespace {
 
@@ -670,7 +670,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             const T rn = sqrt_rn(sums[0]);
             S->r_norm = rn;
             S->r0 = rn;
-            S->h_res[S->n_res++] = static_cast<double>(rn);
+            S->h_res[S->n_res++ & S->hmask] = static_cast<double>(rn);
             if (static_cast<double>(rn) <= S->tau) {
                 S->converged = 1;
                 S->done = 1;
@@ -683,7 +683,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
                 break;
             }
             S->kappa_old = sums[0];
-            S->h_kap[S->n_kap++] = static_cast<double>(sums[0]);
+            S->h_kap[S->n_kap++ & S->hmask] = static_cast<double>(sums[0]);
             if (!(static_cast<double>(sums[0]) > 0.0)) {
                 S->error = kErrKappa;
                 S->done = 1;
@@ -701,7 +701,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             const T al = A::div(S->kappa_old, sums[0]);
             S->alpha = al;
             S->neg_alpha = -al;
-            S->h_alp[S->n_alp++] = static_cast<double>(al);
+            S->h_alp[S->n_alp++ & S->hmask] = static_cast<double>(al);
             if (op == kOpSigma0) {
                 S->it = 1;
             } else if (op == kOpIlSpmv) {
@@ -718,7 +718,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             const T ka = sums[1];
             S->r_norm = rn;
             S->kappa = ka;
-            S->h_res[S->n_res++] = static_cast<double>(rn);
+            S->h_res[S->n_res++ & S->hmask] = static_cast<double>(rn);
             S->iterations = S->it;
             if (static_cast<double>(rn) / static_cast<double>(S->r0) < S->eps ||
                 static_cast<double>(rn) < S->tau) {
@@ -726,16 +726,16 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
                 S->done = 1;
                 break;
             }
-            S->h_kap[S->n_kap++] = static_cast<double>(ka);
+            S->h_kap[S->n_kap++ & S->hmask] = static_cast<double>(ka);
             const T be = A::div(ka, S->kappa_old);
             S->beta = be;
-            S->h_bet[S->n_bet++] = static_cast<double>(be);
+            S->h_bet[S->n_bet++ & S->hmask] = static_cast<double>(be);
             S->kappa_old = ka;
         } break;
         case kOpStdRnorm: {
             const T rn = sqrt_rn(sums[0]);
             S->r_norm = rn;
-            S->h_res[S->n_res++] = static_cast<double>(rn);
+            S->h_res[S->n_res++ & S->hmask] = static_cast<double>(rn);
             S->iterations = S->it;
             if (static_cast<double>(rn) / static_cast<double>(S->r0) < S->eps ||
                 static_cast<double>(rn) < S->tau) {
@@ -751,10 +751,10 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             }
             const T ka = sums[0];
             S->kappa = ka;
-            S->h_kap[S->n_kap++] = static_cast<double>(ka);
+            S->h_kap[S->n_kap++ & S->hmask] = static_cast<double>(ka);
             const T be = A::div(ka, S->kappa_old);
             S->beta = be;
-            S->h_bet[S->n_bet++] = static_cast<double>(be);
+            S->h_bet[S->n_bet++ & S->hmask] = static_cast<double>(be);
             S->kappa_old = ka;
             if (++S->it > S->maxiter) S->done = 1;
         } break;

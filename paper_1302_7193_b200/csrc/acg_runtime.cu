@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <memory>
@@ -297,6 +298,13 @@ struct acg_context {
     void* gather_send = nullptr;  // 4 T (NCCL)
     std::vector<acg_field*> pool; // reusable scratch fields (host entry points)
     acg_solver* cached = nullptr; // solver state reused by acg_solve / acg_solve_host
+    // Serialises every entry point that touches the mutable per-context state
+    // above (scratch pool, cached solver, staging buffers, API scalars, the
+    // stream's reduction buffers). The reference shares OperatorContext
+    // read-only between concurrent solves (operator.hpp:28); here
+    // concurrent calls on one context queue on this lock and run one after
+    // the other on the context's stream, so each sees a consistent state.
+    mutable std::recursive_mutex mu;
     std::unique_ptr<IpcState> ipc; // peer-memory transport (acg_comm_create_ipc)
     size_t s = 8;
     bool fast() const { return math == ACG_MATH_FAST; }
@@ -311,6 +319,11 @@ struct acg_field {
 };
 
 namespace {
+
+struct CtxLock {
+    std::unique_lock<std::recursive_mutex> lk;
+    explicit CtxLock(const acg_context* c) : lk(c->mu) {}
+};
 
 struct DeviceGuard {
     int prev = -1;
@@ -454,7 +467,7 @@ extern "C" {
 
 const char* acg_last_error(void) { return t_err.c_str(); }
 int acg_abi_version(void) { return ACG_ABI_VERSION; }
-long long acg_kernel_launch_count(void) { return g_launches; }
+long long acg_kernel_launch_count(void) { return g_launches.load(); }
 
 acg_status acg_device_count(int* count) {
     return guarded([&] {
@@ -678,11 +691,62 @@ acg_status acg_synchronize(const acg_context* c) {
     return guarded([&] {
         check_ctx(c);
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         CK(cudaStreamSynchronize(c->stream));
     });
 }
 
 void* acg_context_stream(const acg_context* c) { return c ? c->stream : nullptr; }
+
+acg_status acg_context_wait_stream(const acg_context* c, void* stream) {
+    return guarded([&] {
+        check_ctx(c);
+        DeviceGuard g(c->device);
+        CtxLock lk(c);
+        cudaEvent_t e = nullptr;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const cudaError_t r1 = cudaEventRecord(e, static_cast<cudaStream_t>(stream));
+        const cudaError_t r2 = r1 == cudaSuccess ? cudaStreamWaitEvent(c->stream, e, 0) : r1;
+        cudaEventDestroy(e);  // released once the wait is resolved
+        CK(r2);
+    });
+}
+
+acg_status acg_stream_wait_context(void* stream, const acg_context* c) {
+    return guarded([&] {
+        check_ctx(c);
+        DeviceGuard g(c->device);
+        CtxLock lk(c);
+        cudaEvent_t e = nullptr;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const cudaError_t r1 = cudaEventRecord(e, c->stream);
+        const cudaError_t r2 =
+            r1 == cudaSuccess ? cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e, 0) : r1;
+        cudaEventDestroy(e);
+        CK(r2);
+    });
+}
+
+acg_status acg_context_release_scratch(const acg_context* cc) {
+    return guarded([&] {
+        check_ctx(cc);
+        DeviceGuard g(cc->device);
+        CtxLock lk(cc);
+        acg_context* c = const_cast<acg_context*>(cc);
+        CK(cudaStreamSynchronize(c->stream));
+        destroy_cached_solver(c);
+        for (acg_field* f : c->pool) {
+            for (void* b : f->base) cudaFree(b);
+            delete f;
+        }
+        c->pool.clear();
+        for (Slab& s : c->slabs)
+            if (s.staging) {
+                cudaFree(s.staging);
+                s.staging = nullptr;
+            }
+    });
+}
 
 }  // extern "C"
 
@@ -1106,6 +1170,7 @@ acg_status acg_field_create(acg_field** out, const acg_context* c) {
         check_ctx(c);
         if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         *out = new_field(c);
     });
 }
@@ -1114,6 +1179,7 @@ acg_status acg_field_destroy(acg_field* f) {
     return guarded([&] {
         if (!f) return;
         DeviceGuard g(f->ctx->device);
+        CtxLock lk(f->ctx);
         cudaStreamSynchronize(f->ctx->stream);
         free_field(f);
     });
@@ -1125,6 +1191,7 @@ acg_status acg_field_upload(acg_field* f, const void* host, acg_layout layout,
         if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, upload_t<T>(f, host, layout, scope));
     });
 }
@@ -1135,6 +1202,7 @@ acg_status acg_field_download(const acg_field* f, void* host, acg_layout layout,
         if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, download_t<T>(f, host, layout, scope));
     });
 }
@@ -1145,6 +1213,7 @@ acg_status acg_field_upload_device(acg_field* f, const void* dev, acg_layout lay
         if (!f || !dev) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, upload_dev_t<T>(f, dev, layout, scope));
     });
 }
@@ -1155,6 +1224,7 @@ acg_status acg_field_download_device(const acg_field* f, void* dev, acg_layout l
         if (!f || !dev) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, download_dev_t<T>(f, dev, layout, scope));
     });
 }
@@ -1164,6 +1234,7 @@ acg_status acg_field_fill(acg_field* f, double value) {
         if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             for (size_t si = 0; si < c->slabs.size(); ++si)
                 launch_fill<T>(c->slabs[si].n_loc, static_cast<T>(value),
@@ -1178,6 +1249,7 @@ acg_status acg_field_fill_random(acg_field* f, uint64_t seed) {
         if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
         const acg_context* c = f->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             for (size_t si = 0; si < c->slabs.size(); ++si)
                 launch_fill_random<T>(view<T>(c, si), seed, static_cast<T*>(f->data(si)),
@@ -1192,6 +1264,7 @@ acg_status acg_field_copy(acg_field* dst, const acg_field* src) {
         check_same(dst, src, "copy");
         const acg_context* c = dst->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, op_copy<T>(c, src, dst, nullptr));
         CK(cudaPeekAtLastError());
     });
@@ -1204,6 +1277,7 @@ acg_status acg_apply(const acg_context* c, const acg_field* x, acg_field* y) {
         check_field(c, y, "apply");
         if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "apply: x and y must not alias");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, op_apply<T>(c, x, y, nullptr));
         CK(cudaPeekAtLastError());
     });
@@ -1216,6 +1290,7 @@ acg_status acg_precondition(const acg_context* c, const acg_field* y, acg_field*
         check_field(c, x, "precondition");
         if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "precondition: y and x must not alias");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c);
             auto S = tmp_scalars<T>(c);
@@ -1233,6 +1308,7 @@ acg_status acg_axpy(double alpha, const acg_field* x, acg_field* y) {
         check_same(x, y, "axpy");
         const acg_context* c = x->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, op_axpy<T>(c, static_cast<T>(alpha), nullptr, -1, false, x, y, false));
         CK(cudaPeekAtLastError());
     });
@@ -1243,6 +1319,7 @@ acg_status acg_scal(double alpha, acg_field* x) {
         if (!x) fail(ACG_ERR_INVALID_ARGUMENT, "scal: null field");
         const acg_context* c = x->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             for (size_t si = 0; si < c->slabs.size(); ++si)
                 launch_scal<T>(c->slabs[si].n_loc, static_cast<T>(alpha), nullptr,
@@ -1258,6 +1335,7 @@ acg_status acg_dot(const acg_field* x, const acg_field* y, double* out) {
         if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
         const acg_context* c = x->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c);
             auto S = tmp_scalars<T>(c);
@@ -1272,6 +1350,7 @@ acg_status acg_nrm2(const acg_field* x, double* out) {
         if (!x || !out) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = x->ctx;
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c);
             auto S = tmp_scalars<T>(c);
@@ -1289,6 +1368,7 @@ acg_status acg_true_residual(const acg_context* c, const acg_field* u, const acg
         check_field(c, f, "true_residual");
         if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, *out = static_cast<double>(op_true_residual<T>(c, u, f)));
     });
 }
@@ -1302,6 +1382,7 @@ acg_status acg_interleaved_spmv_kernel(const acg_context* c, acg_field* u, acg_f
                                    static_cast<const acg_field*>(q), z})
             check_field(c, f, "interleaved_spmv_kernel");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c, static_cast<T>(alpha), static_cast<T>(beta));
             auto S = tmp_scalars<T>(c);
@@ -1329,6 +1410,7 @@ acg_status acg_interleaved_prec_kernel(const acg_context* c, acg_field* r, acg_f
              {static_cast<const acg_field*>(r), static_cast<const acg_field*>(z), q})
             check_field(c, f, "interleaved_prec_kernel");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c, static_cast<T>(alpha));
             auto S = tmp_scalars<T>(c);
@@ -1351,6 +1433,14 @@ acg_status acg_interleaved_prec_kernel(const acg_context* c, acg_field* r, acg_f
             if (kappa) *kappa = static_cast<double>(h.val[1]);
         });
     });
+}
+
+void acg_solve_result_release(acg_solve_result* res) {
+    if (!res) return;
+    for (double*& h : res->history) {
+        std::free(h);
+        h = nullptr;
+    }
 }
 
 void acg_solver_config_default(acg_solver_config* cfg) {
@@ -1428,7 +1518,9 @@ struct acg_solver {
     void* mirror = nullptr;   // pinned 2 x Scalars<T>
     cudaEvent_t mev[2] = {nullptr, nullptr};
     bool started = false;
-    int cap = 0;              // history capacity (entries)
+    int cap = 0;              // device history ring capacity (entries, power of two)
+    std::vector<double> hv[4];  // host copies of the histories (drained from the rings)
+    int drained[4] = {0, 0, 0, 0};
     long long launches0 = 0;
     EventTimer timer;       // per-family timings (record_timings)
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
@@ -1479,7 +1571,7 @@ std::vector<Scalars<T>*> sv(acg_solver* s) {
 template <typename T>
 void solver_alloc(acg_solver* s) {
     const acg_context* c = s->ctx;
-    const int cap = std::max(s->cfg.maxiter + 2, 4096);
+    const int cap = kHistRing;  // independent of maxiter: the host drains the rings
     s->cap = cap;
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         void* p = nullptr;
@@ -1506,10 +1598,6 @@ void solver_alloc(acg_solver* s) {
 template <typename T>
 acg_solver* cached_solver(const acg_context* c, const acg_solver_config* cfg) {
     acg_context* cc = const_cast<acg_context*>(c);
-    if (cc->cached && cc->cached->cap < cfg->maxiter + 2) {
-        delete cc->cached;
-        cc->cached = nullptr;
-    }
     if (!cc->cached) {
         auto s = std::make_unique<acg_solver>();
         s->ctx = c;
@@ -1526,8 +1614,12 @@ template <typename T>
 void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
     const acg_context* c = s->ctx;
     s->t0 = std::chrono::steady_clock::now();
-    s->launches0 = g_launches;
+    s->launches0 = g_launches.load();
     s->f = f;
+    for (int a = 0; a < 4; ++a) {
+        s->hv[a].clear();
+        s->drained[a] = 0;
+    }
     s->timer.st = c->stream;
     s->ktimer.st = c->stream;
     s->timer.on = s->cfg.record_timings != 0;
@@ -1538,6 +1630,7 @@ void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
         h.tau = s->cfg.tau;
         h.maxiter = s->cfg.maxiter;
         h.it = 1;
+        h.hmask = s->cap - 1;
         h.h_res = s->hist[si * 4 + 0];
         h.h_kap = s->hist[si * 4 + 1];
         h.h_alp = s->hist[si * 4 + 2];
@@ -1733,6 +1826,30 @@ double bytes_per_iteration(const acg_context* c) {
     return static_cast<double>(c->s) * (11.0 * n) / c->nslabs_total;
 }
 
+// Copy history entries [drained, counts) out of the device rings into the
+// host vectors (synchronous). Entries written after `counts` stay in the ring:
+// the caller drains before the device can be a full ring ahead.
+void drain_histories(acg_solver* s, const int counts[4]) {
+    const acg_context* c = s->ctx;
+    const int cap = s->cap;
+    for (int a = 0; a < 4; ++a) {
+        const int lo = s->drained[a], hi = counts[a];
+        if (hi <= lo) continue;
+        if (hi - lo > cap) fail(ACG_ERR_INTERNAL, "history ring overrun (%d entries)", hi - lo);
+        s->hv[a].resize(static_cast<size_t>(hi));
+        int k = lo;
+        while (k < hi) {  // at most two contiguous ring segments
+            const int off = k & (cap - 1);
+            const int n = std::min(hi - k, cap - off);
+            CK(cudaMemcpyAsync(s->hv[a].data() + k, s->hist[a] + off, n * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+            k += n;
+        }
+        s->drained[a] = hi;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+}
+
 // Enqueue iterations in batches; poll the done flag of the batch before the
 // current one (pipelined, so the GPU never idles on the host).
 template <typename T>
@@ -1757,7 +1874,15 @@ void solver_run(acg_solver* s) {
         CK(cudaEventRecord(s->mev[b & 1], c->stream));
         if (b > 0) {
             CK(cudaEventSynchronize(s->mev[(b - 1) & 1]));
-            if (mir[(b - 1) & 1].done) break;
+            const Scalars<T>& m = mir[(b - 1) & 1];
+            if (m.done) break;
+            // the device runs at most two batches (<= 128 entries per history)
+            // ahead of this snapshot: drain well before a ring can wrap onto
+            // undrained entries
+            const int counts[4] = {m.n_res, m.n_kap, m.n_alp, m.n_bet};
+            int most = 0;
+            for (int a = 0; a < 4; ++a) most = std::max(most, counts[a] - s->drained[a]);
+            if (most >= s->cap / 2) drain_histories(s, counts);
         }
         ++b;
     }
@@ -1813,15 +1938,22 @@ void solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, doubl
             res->timings.fused_spmv = s->timer.seconds(kFusedSpmv);
             res->timings.fused_prec = s->timer.seconds(kFusedPrec);
         }
-        res->kernel_launches = g_launches - s->launches0;
+        res->kernel_launches = g_launches.load() - s->launches0;
     }
-    double* outs[4] = {hr, hk, ha, hb};
     const int counts[4] = {h.n_res, h.n_kap, h.n_alp, h.n_bet};
-    for (int a = 0; a < 4; ++a)
-        if (outs[a] && counts[a] > 0)
-            CK(cudaMemcpyAsync(outs[a], s->hist[a], counts[a] * sizeof(double),
-                               cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    drain_histories(s, counts);  // also orders the stream (true residual, u_out)
+    double* outs[4] = {hr, hk, ha, hb};
+    for (int a = 0; a < 4; ++a) {
+        const size_t n = static_cast<size_t>(counts[a]);
+        if (outs[a]) {
+            if (n) std::memcpy(outs[a], s->hv[a].data(), n * sizeof(double));
+        } else if (res) {  // library-owned copy, released by acg_solve_result_release
+            double* d = static_cast<double*>(std::malloc(std::max<size_t>(n, 1) * sizeof(double)));
+            if (!d) throw std::bad_alloc();
+            if (n) std::memcpy(d, s->hv[a].data(), n * sizeof(double));
+            res->history[a] = d;
+        }
+    }
 }
 
 }  // namespace
@@ -1834,6 +1966,7 @@ acg_status acg_solver_create(acg_solver** out, const acg_context* c, const acg_s
         if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
         validate(cfg);
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         auto s = std::make_unique<acg_solver>();
         s->ctx = c;
         s->cfg = *cfg;
@@ -1846,6 +1979,7 @@ acg_status acg_solver_destroy(acg_solver* s) {
     return guarded([&] {
         if (!s) return;
         DeviceGuard g(s->ctx->device);
+        CtxLock lk(s->ctx);
         cudaStreamSynchronize(s->ctx->stream);
         delete s;
     });
@@ -1858,6 +1992,7 @@ acg_status acg_solver_start(acg_solver* s, const acg_field* f, const acg_field* 
         check_field(c, f, "solve");
         if (u0) check_field(c, u0, "solve");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, solver_start<T>(s, f, u0));
     });
 }
@@ -1866,6 +2001,7 @@ acg_status acg_solver_iterate(acg_solver* s, int n) {
     return guarded([&] {
         if (!s || !s->started) fail(ACG_ERR_INVALID_ARGUMENT, "solver not started");
         DeviceGuard g(s->ctx->device);
+        CtxLock lk(s->ctx);
         ACG_TDISPATCH(s->ctx, solver_iterate<T>(s, n));
     });
 }
@@ -1883,6 +2019,7 @@ acg_status acg_solver_kernel_times(acg_solver* s, int* n_prec, double* ms_prec, 
     return guarded([&] {
         if (!s) fail(ACG_ERR_INVALID_ARGUMENT, "null solver");
         DeviceGuard g(s->ctx->device);
+        CtxLock lk(s->ctx);
         CK(cudaStreamSynchronize(s->ctx->stream));
         if (n_prec) *n_prec = s->ktimer.count(kFusedPrec);
         if (ms_prec) *ms_prec = s->ktimer.seconds(kFusedPrec) * 1e3;
@@ -1898,6 +2035,7 @@ acg_status acg_solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* 
         if (!s || !s->started) fail(ACG_ERR_INVALID_ARGUMENT, "solver not started");
         if (u_out) check_field(s->ctx, u_out, "solve");
         DeviceGuard g(s->ctx->device);
+        CtxLock lk(s->ctx);
         ACG_TDISPATCH(s->ctx, solver_finish<T>(s, u_out, res, hr, hk, ha, hb));
     });
 }
@@ -1912,6 +2050,7 @@ acg_status acg_solve(const acg_context* c, const acg_field* f, const acg_field* 
         if (u_out) check_field(c, u_out, "solve");
         validate(cfg);
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         ACG_TDISPATCH(c, {
             acg_solver* s = cached_solver<T>(c, cfg);
             solver_start<T>(s, f, u0);
@@ -1928,6 +2067,7 @@ acg_status acg_apply_host(const acg_context* c, acg_layout layout, const void* x
         if (!x || !y) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
         if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "apply: x and y must not alias");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         PoolField fx(c), fy(c);
         ACG_TDISPATCH(c, {
             upload_t<T>(fx.f, x, layout, ACG_HOST_FULL);
@@ -1943,6 +2083,7 @@ acg_status acg_precondition_host(const acg_context* c, acg_layout layout, const 
         if (!x || !y) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
         if (x == y) fail(ACG_ERR_INVALID_ARGUMENT, "precondition: y and x must not alias");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         PoolField fy(c), fx(c);
         ACG_TDISPATCH(c, {
             upload_t<T>(fy.f, y, layout, ACG_HOST_FULL);
@@ -1964,6 +2105,7 @@ acg_status acg_true_residual_host(const acg_context* c, acg_layout layout, const
         check_ctx(c);
         if (!u || !f || !out) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         PoolField fu(c), ff(c);
         ACG_TDISPATCH(c, {
             upload_t<T>(fu.f, u, layout, ACG_HOST_FULL);
@@ -1981,6 +2123,7 @@ acg_status acg_solve_host(const acg_context* c, acg_layout layout, const void* f
         if (!f || !u_out) fail(ACG_ERR_INVALID_ARGUMENT, "null buffer");
         validate(cfg);
         DeviceGuard g(c->device);
+        CtxLock lk(c);
         PoolField ff(c), fu0(c), fu(c);
         ACG_TDISPATCH(c, {
             upload_t<T>(ff.f, f, layout, ACG_HOST_FULL);

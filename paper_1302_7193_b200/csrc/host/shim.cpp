@@ -83,12 +83,26 @@ std::shared_ptr<acg_context> make_device_context(acg_dtype dtype, const Vertical
     });
 }
 
-// Shape-only contexts for the context-free level-1 API (axpy/scal/dot/nrm2/
-// fill_random take fields, not an operator). Kept for the process lifetime.
-acg_context* shape_context(acg_dtype dtype, int m, int n_z) {
-    static std::mutex mu;
+namespace {
+std::mutex g_shape_mu;
+std::map<std::tuple<int, int, int>, acg_context*>& shape_cache() {
     static auto* cache = new std::map<std::tuple<int, int, int>, acg_context*>();
-    std::lock_guard<std::mutex> lk(mu);
+    return *cache;
+}
+}  // namespace
+
+void release_scratch(const acg_context* c) {
+    drop_pool(c);
+    check(acg_context_release_scratch(c));
+}
+
+// Shape-only contexts for the context-free level-1 API (axpy/scal/dot/nrm2/
+// fill_random take fields, not an operator). The contexts themselves (profile
+// and column tables) live for the process; their field-sized scratch is freed
+// by release_device_scratch().
+acg_context* shape_context(acg_dtype dtype, int m, int n_z) {
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    auto* cache = &shape_cache();
     const auto key = std::make_tuple(static_cast<int>(dtype), m, n_z);
     auto it = cache->find(key);
     if (it != cache->end()) return it->second;
@@ -113,4 +127,20 @@ acg_context* shape_context(acg_dtype dtype, int m, int n_z) {
 }
 
 }  // namespace detail
+
+void release_device_scratch() {
+    std::vector<const acg_context*> pooled;
+    {
+        std::lock_guard<std::mutex> lk(detail::g_mu);
+        for (auto& kv : detail::g_pool) pooled.push_back(kv.first);
+    }
+    for (const acg_context* c : pooled) detail::drop_pool(c);
+    std::vector<acg_context*> ctxs;
+    {
+        std::lock_guard<std::mutex> lk(detail::g_shape_mu);
+        for (auto& kv : detail::shape_cache()) ctxs.push_back(kv.second);
+    }
+    for (acg_context* c : ctxs) detail::release_scratch(c);
+}
+
 }  // namespace anisocg

@@ -172,7 +172,11 @@ void bind_context(py::module_& mod, const char* name) {
             d["bytes_per_field"] = i.bytes_per_field_local;
             d["thomas_tmem"] = static_cast<bool>(i.thomas_tmem);
             return d;
-        });
+        })
+        .def(
+            "release_scratch",
+            [](const OperatorContext<T>& c) { detail::release_scratch(c.device()); },
+            "Free the device scratch cached between calls (re-created on demand)");
     (void)sizeof(Cls);
 }
 
@@ -474,6 +478,8 @@ PYBIND11_MODULE(_anisocg, mod) {
         },
         py::arg("field"), py::kw_only(), py::arg("layout") = "vertical",
         "io::dump_field: text header + raw little-endian values (bytes)");
+    mod.def("release_scratch", &release_device_scratch,
+            "Free the device scratch the context-free level-1 API keeps between calls");
     mod.def("kernel_launch_count", &acg_kernel_launch_count,
             "Device kernels launched by this process through libacg_cuda.so");
 }

@@ -84,8 +84,16 @@ def solve(ctx, f, u0=None, epsilon=1e-5, tau=1e-20, maxiter=500, variant="interl
     if backend != "matrix-free":
         raise ValueError("backend must be 'matrix-free' (the CSR comparison backend is not "
                          "part of the GPU path)")
-    if not (epsilon > 0) or not (tau >= 0) or maxiter < 1:
-        raise ValueError("epsilon must be > 0, tau >= 0 and maxiter >= 1")
+    # SolverConfig::validate (solver.hpp:27-35): the same checks and messages as
+    # the host path
+    if not (epsilon > 0):
+        raise ValueError("SolverConfig: epsilon must be > 0")
+    if not (tau > 0):
+        raise ValueError("SolverConfig: tau must be > 0")
+    if maxiter < 1:
+        raise ValueError("SolverConfig: maxiter must be >= 1")
+    if workers < 1:
+        raise ValueError("SolverConfig: workers must be >= 1")
     L = _layout(layout)
     c = _Ctx(ctx)
     ff = c.field(f, L)

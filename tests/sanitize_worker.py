@@ -1,0 +1,61 @@
+"""Worker for tests/test_sanitizers.py: small solves through every kernel family
+(run under compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck).
+
+Covers the interleaved loop (TMEM Thomas sweep K1 with its cp.async ring and
+tcgen05 alloc/dealloc, the pair stencil sweep K2, fused reduction stage 1 +
+the wide stage-2 tree with PDL early starts), the standard loop (apply,
+precondition, BLAS-1, k_tree1 path), fp32 (k_thomas_tm2 / k_fused_spmv_pair),
+FAST math, the host transfers (K7 transposes), the device RNG, and p = 2
+virtual slabs (halo copies, slab-sum combine). Checks the results against the
+CPU oracle so a sanitizer run is also a parity run.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import paper_1302_7193_b200 as acg  # noqa: E402
+from oracle.oracle import Oracle, Problem  # noqa: E402
+
+CASES = [(32, 16), (256, 6)] if len(sys.argv) < 2 else [
+    tuple(int(x) for x in a.split("x")) for a in sys.argv[1:]]
+
+
+def main():
+    for m, n_z in CASES:
+        prob = Problem(m, n_z)
+        o = Oracle(prob)
+        g = acg.vertical_grid(n_z, prob.h)
+        pro = acg.vertical_profile(g, prob.omega2, prob.lambda2)
+        pan = acg.cubed_sphere_panel(m)
+        for dt, cls in ((np.float64, acg.OperatorContext), (np.float32, acg.OperatorContextF32)):
+            for math, slabs in (("exact", 1), ("fast", 1), ("exact", 2)):
+                ctx = cls(pro, pan, math=math, slabs=slabs)
+                f = o.random_field(42, dt)
+                eps = 1e-8 if dt == np.float64 else 1e-4
+                for variant in ("interleaved", "standard"):
+                    u, r = acg.solve(ctx, f, epsilon=eps, maxiter=40, variant=variant)
+                    if math == "exact":
+                        uo, ro = o.solve(f, epsilon=eps, maxiter=40, variant=variant)
+                        assert r.iterations == ro.iterations, (m, n_z, dt, variant)
+                        assert np.array_equal(r.residual_history, ro.residual_history)
+                        assert np.array_equal(u, uo)
+                x = o.random_field(5, dt)
+                y = acg.apply(ctx, x)
+                z = acg.precondition(ctx, x)
+                acg.true_residual(ctx, x, f)
+                if math == "exact":
+                    assert np.array_equal(y, o.apply(x)) and np.array_equal(z, o.precondition(x))
+                h = acg.apply(ctx, np.ascontiguousarray(np.transpose(x, (1, 2, 0))),
+                              layout="horizontal")
+                assert np.array_equal(np.transpose(h, (2, 0, 1)), y)
+            assert np.array_equal(acg.random_field(m, n_z, 42), o.random_field(42))
+        print(f"case {m}x{n_z} ok", flush=True)
+    print("SANITIZE_DONE", flush=True)
+
+
+if __name__ == "__main__":
+    main()

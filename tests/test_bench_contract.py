@@ -76,3 +76,32 @@ def test_gpu_arm_json_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 4 * d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,config", [(2, "c1"), (4, "c1")])
+def test_gpu_arm_multi_rank_reexec(n, config):
+    """`python bench.py --gpus N` outside torchrun relaunches itself as N ranks
+    (here all on GPU 0: ACG_SAME_GPU=1, peer-memory transport), reports
+    n_gpus = N and verifies the N-rank residual history against the same
+    iterations on one GPU, bit for bit (the slabs are reduction-tree nodes)."""
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            pytest.skip("no GPU")
+    except Exception:
+        pytest.skip("no torch")
+    env = dict(os.environ, OMP_NUM_THREADS="2", ACG_SAME_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n),
+                        "--config", config, "--steps", "5", "--warmup", "3", "--no-cpu",
+                        "--no-e2e", "--sustain-steps", "20"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == n and d["exact_tree"] is True
+    v = d["verified_vs_1gpu"]
+    assert v["ok"] is True and v["exact_tree"] is True and v["max_dev_over_r0"] == 0.0
+    assert d["sustained"]["steps"] == 20 and d["sustained"]["value"] > 0

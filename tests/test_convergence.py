@@ -1,0 +1,114 @@
+"""Convergence-to-epsilon parity at the BASELINE sizes against the reference.
+
+north_star: "same iteration count to convergence (±1), residual history within
+1e-10 relative in fp64 (1e-4 in fp32), and final solution within the stated
+relative tolerance". The reference's own solves (oracle/_ref: the unmodified
+proj/include/anisocg headers + src/grid.cpp + src/profile.cpp, OpenMP on all
+host cores) at these sizes take minutes (C3: 664 iterations, ~320 s on 8 cores),
+so tests/golden/make_convergence.py ran them once and committed the outputs:
+full histories, iteration counts, true residuals, sha256 of u's bytes, max|u|
+and u at 65536 seeded positions.
+
+EXACT math mode: iterations, all four histories and the true residual equal,
+and u bit-identical (sha256 of the whole field). FAST mode (FMA contraction,
+one reciprocal per Thomas level): iterations ±1, residual history within
+1e-10·||r0|| (fp64) / 1e-4·||r0|| (fp32) over the common prefix
+(test_solver.cpp:108-109 normalisation), max|du|/max|u| within the same bound
+on the sampled positions (verify.cpp:31-39 field_rel_diff), and the true
+residual within 1e-9·||r0|| (test_solver.cpp:112-113).
+
+Cases (cubed sphere, omega2 = 6.71e-4, H = 1e-2, RHS seed 42, u0 = 0):
+  c2_il   fp64 512^2 x 128, eps 1e-10, interleaved  (338 iterations)
+  c2_std  fp64 512^2 x 128, eps 1e-10, standard     (338 iterations)
+  c3_il   fp64 1024^2 x 128, eps 1e-10, interleaved (664 iterations; the headline config)
+  c4_il20 fp32 2048^2 x 128, lambda2 = 100, 20 fixed iterations
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden", "convergence_golden.npz")
+
+
+CASES = {
+    "c2_il": dict(m=512, n_z=128, f32=False, lambda2=3.32e-2,
+                  kw=dict(epsilon=1e-10, maxiter=2000, variant="interleaved")),
+    "c2_std": dict(m=512, n_z=128, f32=False, lambda2=3.32e-2,
+                   kw=dict(epsilon=1e-10, maxiter=2000, variant="standard")),
+    "c3_il": dict(m=1024, n_z=128, f32=False, lambda2=3.32e-2,
+                  kw=dict(epsilon=1e-10, maxiter=2000, variant="interleaved")),
+    "c4_il20": dict(m=2048, n_z=128, f32=True, lambda2=1.0e2,
+                    kw=dict(epsilon=1e-300, tau=1e-300, maxiter=20, variant="interleaved")),
+}
+
+
+def sample_index(n):
+    # identical to tests/golden/make_convergence.py:sample_index
+    return np.sort(np.random.default_rng(20260214).choice(n, size=min(65536, n), replace=False))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+def _solve(acg, c, math):
+    g = acg.vertical_grid(c["n_z"], 1e-2)
+    pro = acg.vertical_profile(g, 6.71e-4, c["lambda2"])
+    cls = acg.OperatorContextF32 if c["f32"] else acg.OperatorContext
+    ctx = cls(pro, acg.cubed_sphere_panel(c["m"]), math=math)
+    f = acg.random_field(c["m"], c["n_z"], 42, dtype="float32" if c["f32"] else "float64")
+    u, res = acg.solve(ctx, f, **c["kw"])
+    ctx.release_scratch()
+    return f, u, res
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_converged_solve_bit_exact(acg, gold, case):
+    c = CASES[case]
+    f, u, res = _solve(acg, c, "exact")
+    assert sha(f) == str(gold[f"{case}_f_sha"])          # device RNG == fill_random(42)
+    it, conv, tr = gold[f"{case}_meta"]
+    assert res.iterations == int(it) and res.converged == bool(conv)
+    for key, name in (("res", "residual_history"), ("kap", "kappa_history"),
+                      ("alp", "alpha_history"), ("bet", "beta_history")):
+        assert np.array_equal(getattr(res, name), gold[f"{case}_{key}"]), name
+    assert res.true_residual == tr
+    assert sha(u) == str(gold[f"{case}_u_sha"])           # the whole solution, bit for bit
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_converged_solve_fast_math_tolerance(acg, gold, case):
+    c = CASES[case]
+    tol = 1e-4 if c["f32"] else 1e-10
+    _, u, res = _solve(acg, c, "fast")
+    it = int(gold[f"{case}_meta"][0])
+    assert abs(res.iterations - it) <= 1
+    ref = gold[f"{case}_res"]
+    r0 = ref[0]
+    n = min(len(ref), len(res.residual_history))
+    dev = np.abs(res.residual_history[:n] - ref[:n]).max() / r0
+    assert dev <= tol, dev
+    flat = u.reshape(-1)
+    du = np.abs(flat[sample_index(flat.size)].astype(np.float64) - gold[f"{case}_u_sample"]).max()
+    assert du / float(gold[f"{case}_u_max"]) <= tol
+    assert abs(np.abs(flat).max() - float(gold[f"{case}_u_max"])) <= tol * float(gold[f"{case}_u_max"])
+    assert abs(res.true_residual - gold[f"{case}_meta"][2]) <= (1e-9 if not c["f32"] else 1e-4) * r0
+
+
+def test_fixture_is_the_reference_iteration_count(gold):
+    """SURVEY §6 probe counts at eps = 1e-10: C2 338, C3 664 (both variants)."""
+    assert int(gold["c2_il_meta"][0]) == 338 and int(gold["c2_std_meta"][0]) == 338
+    assert int(gold["c3_il_meta"][0]) == 664
+    assert len(gold["c3_il_res"]) == 665 and len(gold["c3_il_bet"]) == 663

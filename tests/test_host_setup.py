@@ -70,7 +70,7 @@ def test_c_abi_exports_every_declared_symbol():
     lib = ctypes.CDLL(capi.LIB_PATH)
     missing = [s for s in sorted(declared) if not hasattr(lib, s)]
     assert not missing, missing
-    assert capi.lib().acg_abi_version() == 1
+    assert capi.lib().acg_abi_version() == 2
 
 
 def test_partition_plan_is_tree_aligned():
