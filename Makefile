@@ -43,7 +43,7 @@ $(PYMOD): $(CSRC)/python/bindings.cpp $(HOSTSRC) $(HDRS) $(LIB)
 	g++ $(CXXFLAGS) -shared -I$(PYINC) -I$(PBINC) -o $@ $(CSRC)/python/bindings.cpp $(HOSTSRC) \
 	    -L$(PKG) -lacg_cuda -Wl,-rpath,'$$ORIGIN'
 
-oracle:
+oracle: lib
 	$(MAKE) -C oracle PY=$(PY)
 
 clean:

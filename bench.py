@@ -90,7 +90,17 @@ def algorithmic_bytes(cfg, s):
     return {"fused_prec": s * (4 * N + 2 * m * m), "fused_spmv": s * (7 * N + 6 * m * m),
             "iteration": s * (11 * N + 8 * m * m),
             # unfused (standard) loop: apply 2, precondition 2, BLAS-1 16 refs
-            "iteration_standard": s * (20 * N + 8 * m * m)}
+            "iteration_standard": s * (20 * N + 8 * m * m),
+            # matrix-explicit standard loop (backend csr): spmv reads row_ptr (8 B/row),
+            # every entry (value + 32-bit column), x once, writes y; the stored
+            # tridiagonal solve reads dl, dd, du, y and writes x; BLAS-1 16 refs
+            "iteration_csr": 8 * N + csr_nnz(m, n_z) * (s + 4) + s * (2 * N + 5 * N + 16 * N)}
+
+
+def csr_nnz(m, n_z):
+    """Entries of assemble_csr's matrix: every row plus its in-panel neighbours."""
+    N = m * m * n_z
+    return N + 4 * (m - 1) * m * n_z + 2 * (n_z - 1) * m * m
 
 
 def peaks():
@@ -222,6 +232,7 @@ def workload(cfg, args, n):
                         f"interleaved matrix-free PCG (paper Alg. 1-3)",
             "m": cfg["m"], "n_z": cfg["n_z"], "omega2": OMEGA2, "lambda2": cfg["lambda2"],
             "h_atmos": H, "seed": 42, "math": args.math, "variant": args.variant,
+            "backend": args.backend,
             "parallelism": (f"{n} i-slabs, one per GPU, {args.transport} transport" if n > 1
                             else "1 GPU"),
             "l2": "no flush: every field (N*s bytes) exceeds the 126 MB L2"}
@@ -243,7 +254,8 @@ def verify_against_one_gpu(args, cfg, rank, world, dev, res, info, dtype, math_m
         c1 = capi.Context.from_setup(profile, panel, dtype=dtype, math=math_mode, device=dev)
         f1 = c1.field().fill_random(42)
         r1 = capi.solve(c1, f1, epsilon=1e-300, tau=1e-300, maxiter=max(len(hist) - 1, 1),
-                        variant=variant)
+                        variant=variant,
+                        backend=capi.CSR if args.backend == "csr" else capi.MATRIX_FREE)
         h1 = r1["residual_history"]
         exact = bool(info["exact_tree"])
         same_len = len(h1) == len(hist)
@@ -330,9 +342,10 @@ def run_gpu(args, cfg):
 
     f = ctx.field().fill_random(42)
     variant = capi.INTERLEAVED if args.variant == "interleaved" else capi.STANDARD
+    backend = capi.CSR if args.backend == "csr" else capi.MATRIX_FREE
     solver = capi.Solver(ctx, epsilon=1e-300, tau=1e-300,
                          maxiter=args.warmup + 3 * args.steps + args.sustain_steps + 8,
-                         variant=variant)
+                         variant=variant, backend=backend)
     solver.start(f)
     solver.iterate(args.warmup)
     ctx.sync()
@@ -437,10 +450,13 @@ def run_gpu(args, cfg):
             "fused_prec_ms": t1 / max(n1, 1), "fused_spmv_ms": t2 / max(n2, 1),
             "fused_prec_gbs": ab["fused_prec"] * local_frac / (t1 / n1 * 1e-3) / 1e9 if n1 and t1 else None,
             "fused_spmv_gbs": ab["fused_spmv"] * local_frac / (t2 / n2 * 1e-3) / 1e9 if n2 and t2 else None}
-    iter_bytes = ab["iteration_standard" if args.variant == "standard" else "iteration"]
+    iter_bytes = ab["iteration_csr" if args.backend == "csr" else
+                    "iteration_standard" if args.variant == "standard" else "iteration"]
     iter_gbs = iter_bytes * it_s / 1e9
     if args.variant == "standard":  # no K1/K2 launches: roofline at the iteration level
-        roof.update({"kernel": "iteration (standard loop, 9 sweeps)", "achieved": iter_gbs,
+        kname = ("iteration (matrix-explicit standard loop: CSR spmv + stored tridiagonals "
+                 "+ BLAS-1)" if args.backend == "csr" else "iteration (standard loop, 9 sweeps)")
+        roof.update({"kernel": kname, "achieved": iter_gbs,
                      "frac": iter_gbs / pk["hbm_gbs"], "traffic": None,
                      "algorithmic_bytes_per_launch": iter_bytes, "launch_ms": ms_max / args.steps})
 
@@ -457,7 +473,7 @@ def run_gpu(args, cfg):
         # one untimed warm-up call (allocates the context's cached solver state)
         f2.upload(hf.array, scope=capi.HOST_LOCAL)
         capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps,
-                         variant=variant)
+                   variant=variant, backend=backend)
         u2.download(out=hu.array, scope=capi.HOST_LOCAL)
         barrier()
         t0 = time.perf_counter()
@@ -465,7 +481,7 @@ def run_gpu(args, cfg):
         ctx.sync()
         t1 = time.perf_counter()
         r2 = capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps,
-                         variant=variant)
+                        variant=variant, backend=backend)
         t2 = time.perf_counter()
         u2.download(out=hu.array, scope=capi.HOST_LOCAL)
         barrier()
@@ -534,6 +550,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--math", default="exact", choices=["exact", "fast"])
     ap.add_argument("--variant", default="interleaved", choices=["interleaved", "standard"])
+    ap.add_argument("--backend", default="matrix-free", choices=["matrix-free", "csr"],
+                    help="csr: the reference's CsrBackend on the GPU (stored matrix + "
+                         "tridiagonals, standard loop) for the matrix-free vs explicit study")
     ap.add_argument("--slabs", type=int, default=1, help="virtual slabs on one GPU (N=1)")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 halo/reduction transport: peer-memory mailboxes (CUDA IPC over "
@@ -549,6 +568,8 @@ def main():
     ap.add_argument("--ktime-inline", action="store_true",
                     help="time K1/K2 launches inside the headline timed region itself")
     args = ap.parse_args()
+    if args.backend == "csr":
+        args.variant = "standard"  # CsrBackend drives the standard loop (solver.hpp:126-154)
     cfg = CONFIGS[args.config]
     if args.impl == "ours" and args.gpus > 1 and int(os.environ.get("WORLD_SIZE", 1)) < args.gpus:
         reexec_under_torchrun(args.gpus)

@@ -202,9 +202,14 @@ typedef struct {
     double tau;      /* absolute tolerance, default 1e-20 */
     int maxiter;     /* default 500 */
     int variant;     /* acg_variant */
-    int backend;     /* acg_backend; only MATRIX_FREE is implemented on the GPU */
+    int backend;     /* acg_backend: MATRIX_FREE, or CSR = the reference's CsrBackend
+                        (solver.hpp:126-145; standard variant only): stencil stored as CSR
+                        plus stored tridiagonals, assembled on the device on first use */
     int workers;     /* accepted and ignored (OpenMP threads in the reference) */
     int record_timings; /* 1: per-kernel-family CUDA-event times in acg_solve_result */
+    int layout;      /* acg_layout of the caller's fields; orders the CSR rows and entries
+                        like assemble_csr(ctx, f.layout()) (csr.hpp:92-124), hence the
+                        CSR summation order. acg_solve_host uses its layout argument. */
 } acg_solver_config;
 
 typedef struct { /* seconds, solver.hpp:39-47 */

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "acg.h"
+#include "anisocg/csr.hpp"
 #include "anisocg/field.hpp"
 #include "anisocg/operator.hpp"
 
@@ -66,6 +67,17 @@ T true_residual(const OperatorContext<T>& ctx, const Field3D<T>& u, const Field3
     return static_cast<T>(out);
 }
 
+/// solver.hpp:71-78 — ||f - A u|| with a stored matrix (host spmv_csr, then
+/// the device level-1 operations of field.hpp)
+template <typename T>
+T true_residual(const CsrMatrix<T>& A, const Field3D<T>& u, const Field3D<T>& f, int workers = 1) {
+    Field3D<T> t(u.m(), u.n_z(), u.layout());
+    spmv_csr(A, u, t, workers);
+    scal(T(-1), t, workers);
+    axpy(T(1), f, t, workers);
+    return nrm2(t, workers);
+}
+
 namespace detail {
 template <typename T>
 std::pair<Field3D<T>, SolveResult> run_solve(const OperatorContext<T>& ctx, const Field3D<T>& f,
@@ -75,9 +87,6 @@ std::pair<Field3D<T>, SolveResult> run_solve(const OperatorContext<T>& ctx, cons
     require_conformant(f, u0, what);
     if (f.m() != ctx.m() || f.n_z() != ctx.n_z())
         throw std::invalid_argument(std::string(what) + ": fields do not match operator context");
-    if (cfg.backend == BackendKind::csr)
-        throw std::invalid_argument(
-            "SolverConfig: the CSR backend is not part of the B200 build (matrix-free only)");
     acg_solver_config c{};
     acg_solver_config_default(&c);
     c.epsilon = cfg.epsilon;
@@ -85,6 +94,9 @@ std::pair<Field3D<T>, SolveResult> run_solve(const OperatorContext<T>& ctx, cons
     c.maxiter = cfg.maxiter;
     c.workers = cfg.workers;
     c.variant = variant == Variant::interleaved ? ACG_VARIANT_INTERLEAVED : ACG_VARIANT_STANDARD;
+    // CsrBackend (solver.hpp:126-145): stored CSR + tridiagonals on the GPU
+    c.backend = cfg.backend == BackendKind::csr ? ACG_BACKEND_CSR : ACG_BACKEND_MATRIX_FREE;
+    c.layout = layout_of(f.layout());
     c.record_timings = 1;
     Field3D<T> u(f.m(), f.n_z(), f.layout());
     acg_solve_result r{};

@@ -404,15 +404,20 @@ class Reference:
                                            _ptr(np.ascontiguousarray(f)), C.byref(out), self.workers))
         return out.value
 
-    def solve(self, f, u0=None, epsilon=1e-5, tau=1e-20, maxiter=500, variant="interleaved", layout=0):
+    def solve(self, f, u0=None, epsilon=1e-5, tau=1e-20, maxiter=500, variant="interleaved", layout=0,
+              backend="matrix-free"):
         f = np.ascontiguousarray(f)
         u = np.empty_like(f)
         cap = maxiter + 2
         hs = [np.zeros(cap) for _ in range(4)]
         res = _RefResult()
+        if backend == "csr" and variant != "standard":
+            raise ValueError("SolverConfig: the interleaved variant exists for the matrix-free "
+                             "backend only")
+        code = 2 if backend == "csr" else (1 if variant == "interleaved" else 0)
         _check(ref_lib().ref_solve(self._h, self._dt(f), layout, _ptr(f),
                                    _ptr(np.ascontiguousarray(u0) if u0 is not None else None),
-                                   epsilon, tau, maxiter, 1 if variant == "interleaved" else 0,
+                                   epsilon, tau, maxiter, code,
                                    self.workers, _ptr(u), C.byref(res), *hs))
         t = {k: getattr(res, k) for k in ("fused_prec_s", "fused_spmv_s", "spmv_s", "prec_s",
                                           "blas_s", "setup_s", "total_s")}

@@ -272,7 +272,8 @@ int ref_true_residual(void* cp, int dtype, int layout, const void* u, const void
     });
 }
 
-// variant: 0 standard, 1 interleaved. Histories are written into caller
+// variant: 0 standard, 1 interleaved, 2 standard on the CsrBackend
+// (backend = csr, solver.hpp:126-145). Histories are written into caller
 // buffers of capacity maxiter + 2; u0 may be null (zero start).
 int ref_solve(void* cp, int dtype, int layout, const void* f, const void* u0, double epsilon,
               double tau, int maxiter, int variant, int workers, void* u_out, ref_result* res,
@@ -286,6 +287,7 @@ int ref_solve(void* cp, int dtype, int layout, const void* f, const void* u0, do
             cfg.maxiter = maxiter;
             cfg.workers = workers;
             cfg.variant = variant == 1 ? Variant::interleaved : Variant::standard;
+            cfg.backend = variant == 2 ? BackendKind::csr : BackendKind::matrix_free;
             auto ff = in_field<T>(c, layout, f);
             Field3D<T> uu(c.geometry.m, c.vgrid.n_z, lay(layout));
             if (u0) uu = in_field<T>(c, layout, u0);

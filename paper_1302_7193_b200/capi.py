@@ -19,6 +19,7 @@ F64, F32 = 0, 1
 VERTICAL, HORIZONTAL = 0, 1
 HOST_FULL, HOST_LOCAL = 0, 1
 STANDARD, INTERLEAVED = 0, 1
+MATRIX_FREE, CSR = 0, 1
 EXACT, FAST = 0, 1
 
 
@@ -52,7 +53,7 @@ class ContextInfo(C.Structure):
 class SolverConfig(C.Structure):
     _fields_ = [("epsilon", C.c_double), ("tau", C.c_double), ("maxiter", C.c_int),
                 ("variant", C.c_int), ("backend", C.c_int), ("workers", C.c_int),
-                ("record_timings", C.c_int)]
+                ("record_timings", C.c_int), ("layout", C.c_int)]
 
 
 class KernelTimings(C.Structure):
@@ -441,11 +442,13 @@ def fused_prec(ctx, r, z, q, alpha):
     return rn.value, ka.value
 
 
-def config(epsilon=1e-5, tau=1e-20, maxiter=500, variant=INTERLEAVED, timings=False):
+def config(epsilon=1e-5, tau=1e-20, maxiter=500, variant=INTERLEAVED, timings=False,
+           backend=MATRIX_FREE, layout=VERTICAL):
     c = SolverConfig()
     lib().acg_solver_config_default(C.byref(c))
     c.epsilon, c.tau, c.maxiter, c.variant = epsilon, tau, maxiter, variant
     c.record_timings = 1 if timings else 0
+    c.backend, c.layout = backend, layout
     return c
 
 

@@ -76,7 +76,8 @@ enum ErrCode { kErrNone = 0,
                kErrPivotFused = 1,    // interleaved_prec_kernel zero pivot
                kErrPivotPrecond = 2,  // precondition zero pivot
                kErrKappa = 3,         // <r,z> not positive
-               kErrSigma = 4 };       // <p,Ap> not positive
+               kErrSigma = 4,         // <p,Ap> not positive
+               kErrPivotTridiag = 5 };// solve_tridiag_set zero pivot (CSR backend)
 
 // Device-resident CG scalars and loop control (FusedState<T> scalars,
 // operator.hpp:195-208, plus the driver state of solver.hpp:275-370).
@@ -88,7 +89,7 @@ struct Scalars {
     int maxiter, it, iterations;
     int done, converged, error;
     int n_res, n_kap, n_alp, n_bet;
-    int pivot;  // written by the Thomas kernels on a zero pivot
+    int pivot;  // written by the Thomas kernels on a zero pivot (2: stored tridiagonals)
     int hmask;  // history arrays are rings of hmask + 1 entries (the host drains them)
     double* h_res;
     double* h_kap;
@@ -193,6 +194,19 @@ template <typename T>
 void launch_fill(long long n, T value, T* x, cudaStream_t st);
 template <typename T>
 void launch_fill_random(const SlabView<T>& v, uint64_t seed, T* x, cudaStream_t st);
+
+// Matrix-explicit backend (acg_csr.cuh): device assembly of the CSR matrix
+// (rows in device order, entries in the caller layout's order) and of the
+// stored tridiagonals; spmv_csr; solve_tridiag_set.
+template <typename T>
+void launch_csr_assemble(const SlabView<T>& v, int horizontal, long long* row_ptr, int* col_idx,
+                         T* vals, T* dl, T* dd, T* du, cudaStream_t st);
+template <typename T>
+void launch_csr_spmv(const SlabView<T>& v, const long long* row_ptr, const int* col_idx,
+                     const T* vals, const T* x, T* y, const Scalars<T>* gate, cudaStream_t st);
+template <typename T>
+void launch_csr_tridiag(const SlabView<T>& v, const T* dl, const T* dd, const T* du, const T* y,
+                        T* x, T* phi, Scalars<T>* flag, const Scalars<T>* gate, cudaStream_t st);
 
 // Reductions: nv (<= 3) arrays of plan.n values -> slab sums.
 //  stage 1: blocks x nv partial node sums into `stage`.

@@ -678,7 +678,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
         } break;
         case kOpKappa0: {
             if (S->pivot) {
-                S->error = kErrPivotPrecond;
+                S->error = S->pivot == 2 ? kErrPivotTridiag : kErrPivotPrecond;
                 S->done = 1;
                 break;
             }
@@ -745,7 +745,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
         } break;
         case kOpStdKappa: {
             if (S->pivot) {
-                S->error = kErrPivotPrecond;
+                S->error = S->pivot == 2 ? kErrPivotTridiag : kErrPivotPrecond;
                 S->done = 1;
                 break;
             }
@@ -1428,6 +1428,8 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
 
 }  // namespace
 
+#include "acg_csr.cuh"
+
 TreePlan make_tree_plan(long long n) {
     TreePlan p{};
     p.n = n;
@@ -1886,7 +1888,14 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
     template void launch_finish<T>(const T*, int, int, bool, Scalars<T>*, int, cudaStream_t,    \
                                    const unsigned long long*, unsigned long long);              \
     template void launch_transpose<T>(const T*, T*, int, int, int, long long, long long,        \
-                                      long long, long long, cudaStream_t);
+                                      long long, long long, cudaStream_t);                      \
+    template void launch_csr_assemble<T>(const SlabView<T>&, int, long long*, int*, T*, T*, T*, \
+                                         T*, cudaStream_t);                                     \
+    template void launch_csr_spmv<T>(const SlabView<T>&, const long long*, const int*, const T*, \
+                                     const T*, T*, const Scalars<T>*, cudaStream_t);            \
+    template void launch_csr_tridiag<T>(const SlabView<T>&, const T*, const T*, const T*,       \
+                                        const T*, T*, T*, Scalars<T>*, const Scalars<T>*,       \
+                                        cudaStream_t);
 
 ACG_INSTANTIATE(double)
 ACG_INSTANTIATE(float)

@@ -262,7 +262,26 @@ struct Slab {
     TreePlan plan{};
     bool tm_ok = false;   // TMEM Thomas sweep usable (validate_thomas_tm)
     int* fin_counter = nullptr;  // last-CTA finish counter of the fused sweeps (zero at rest)
+    // matrix-explicit backend (acg_csr.cuh), assembled on first use per layout
+    int csr_layout = -1;
+    long long* csr_rp = nullptr;
+    int* csr_ci = nullptr;
+    void* csr_val = nullptr;
+    void* tri[3] = {nullptr, nullptr, nullptr};  // dl, dd, du (plane-major)
+    void* tri_phi = nullptr;
 };
+
+void free_csr(Slab& s) {
+    void* ps[] = {s.csr_rp, s.csr_ci, s.csr_val, s.tri[0], s.tri[1], s.tri[2], s.tri_phi};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    s.csr_rp = nullptr;
+    s.csr_ci = nullptr;
+    s.csr_val = nullptr;
+    s.tri[0] = s.tri[1] = s.tri[2] = nullptr;
+    s.tri_phi = nullptr;
+    s.csr_layout = -1;
+}
 
 size_t dsize(acg_dtype t) { return t == ACG_F32 ? sizeof(float) : sizeof(double); }
 
@@ -412,6 +431,7 @@ void build_slab_tables(const acg_context* c, Slab& s, const acg_operator_desc* d
 }
 
 void free_slab(Slab& s) {
+    free_csr(s);
     void* ps[] = {s.prof, s.col, s.part[0], s.part[1], s.part[2], s.stage, s.phi, s.staging, s.tmp,
                   s.fin_counter};
     for (void* p : ps)
@@ -740,11 +760,13 @@ acg_status acg_context_release_scratch(const acg_context* cc) {
             delete f;
         }
         c->pool.clear();
-        for (Slab& s : c->slabs)
+        for (Slab& s : c->slabs) {
             if (s.staging) {
                 cudaFree(s.staging);
                 s.staging = nullptr;
             }
+            free_csr(s);
+        }
     });
 }
 
@@ -1129,6 +1151,68 @@ void op_copy(const acg_context* c, const acg_field* x, acg_field* y, const std::
                        static_cast<T*>(y->data(si)), gS ? (*gS)[si] : nullptr, c->stream);
 }
 
+// ---------------------------------------------------- matrix-explicit backend
+// CsrBackend (solver.hpp:126-145): the CSR matrix and the stored tridiagonals,
+// assembled on the device the first time a solve asks for them (rows ordered
+// for `layout`, csr.hpp:92-124) and kept until release_scratch.
+template <typename T>
+void ensure_csr(const acg_context* cc, int layout) {
+    acg_context* c = const_cast<acg_context*>(cc);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        Slab& s = c->slabs[si];
+        if (s.csr_layout == layout) continue;
+        free_csr(s);
+        if (s.n_loc + 2 * s.plane >= (1ll << 31))
+            fail(ACG_ERR_INVALID_ARGUMENT,
+                 "csr backend: %lld rows per slab exceed the 32-bit column index of CsrMatrix",
+                 s.n_loc);
+        const long long m = c->m, n_z = c->n_z;
+        // nnz of the slab's planes: every row has itself plus its in-panel neighbours
+        long long nnz = 0;
+        for (int il = 0; il < s.m_loc; ++il) {
+            const int i = s.i0 + il;
+            const long long ci = (i > 0) + (i + 1 < m);
+            nnz += n_z * m * (1 + ci) + n_z * (m > 1 ? 2 * (m - 1) : 0) +
+                   m * (n_z > 1 ? 2 * (n_z - 1) : 0);
+        }
+        CK(cudaMalloc(&s.csr_rp, (s.n_loc + 1) * sizeof(long long)));
+        CK(cudaMalloc(&s.csr_ci, nnz * sizeof(int)));
+        CK(cudaMalloc(&s.csr_val, nnz * sizeof(T)));
+        for (void*& t : s.tri) CK(cudaMalloc(&t, s.n_loc * sizeof(T)));
+        CK(cudaMalloc(&s.tri_phi, s.n_loc * sizeof(T)));
+        launch_csr_assemble<T>(view<T>(c, si), layout == ACG_LAYOUT_HORIZONTAL ? 1 : 0, s.csr_rp,
+                               s.csr_ci, static_cast<T*>(s.csr_val), static_cast<T*>(s.tri[0]),
+                               static_cast<T*>(s.tri[1]), static_cast<T*>(s.tri[2]), c->stream);
+        CK(cudaPeekAtLastError());
+        s.csr_layout = layout;
+    }
+}
+
+// spmv_csr (csr.hpp:127-141)
+template <typename T>
+void op_spmv_csr(const acg_context* c, const acg_field* x, acg_field* y, const Scalars<T>* gate) {
+    halo(c, x);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        launch_csr_spmv<T>(view<T>(c, si), s.csr_rp, s.csr_ci, static_cast<const T*>(s.csr_val),
+                           static_cast<const T*>(x->data(si)), static_cast<T*>(y->data(si)), gate,
+                           c->stream);
+    }
+}
+
+// solve_tridiag_set (csr.hpp:175-221)
+template <typename T>
+void op_tridiag(const acg_context* c, const acg_field* y, acg_field* x,
+                const std::vector<Scalars<T>*>& flag, const Scalars<T>* gate) {
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+        const Slab& s = c->slabs[si];
+        launch_csr_tridiag<T>(view<T>(c, si), static_cast<const T*>(s.tri[0]),
+                              static_cast<const T*>(s.tri[1]), static_cast<const T*>(s.tri[2]),
+                              static_cast<const T*>(y->data(si)), static_cast<T*>(x->data(si)),
+                              static_cast<T*>(s.tri_phi), flag[si], gate, c->stream);
+    }
+}
+
 template <typename T>
 T op_true_residual(const acg_context* c, const acg_field* u, const acg_field* f) {
     halo(c, u);
@@ -1141,6 +1225,21 @@ T op_true_residual(const acg_context* c, const acg_field* u, const acg_field* f)
     reduce<T>(c, 1, kOpStore, S, nullptr, false);
     const Scalars<T> h = read_scalars<T>(c, S[0]);
     return std::sqrt(h.val[0]);  // nrm2's sqrt in T (field.hpp:172)
+}
+
+// true_residual(CsrMatrix, u, f), solver.hpp:71-78: t = A u; t = -t; t += f; ||t||
+template <typename T>
+T op_true_residual_csr(const acg_context* c, const acg_field* u, const acg_field* f, acg_field* t) {
+    op_spmv_csr<T>(c, u, t, nullptr);
+    for (size_t si = 0; si < c->slabs.size(); ++si)
+        launch_scal<T>(c->slabs[si].n_loc, T(-1), nullptr, static_cast<T*>(t->data(si)), nullptr,
+                       c->stream);
+    op_axpy<T>(c, T(1), nullptr, -1, false, f, t, false);
+    auto S = tmp_scalars<T>(c);
+    reset_tmp<T>(c);
+    op_dot<T>(c, t, t, kOpStore, S, false);
+    const Scalars<T> h = read_scalars<T>(c, S[0]);
+    return std::sqrt(h.val[0]);
 }
 
 void check_same(const acg_field* a, const acg_field* b, const char* what) {
@@ -1452,6 +1551,7 @@ void acg_solver_config_default(acg_solver_config* cfg) {
     cfg->backend = ACG_BACKEND_MATRIX_FREE;
     cfg->workers = 1;
     cfg->record_timings = 0;
+    cfg->layout = ACG_LAYOUT_VERTICAL;
 }
 
 }  // extern "C"
@@ -1525,7 +1625,9 @@ struct acg_solver {
     EventTimer timer;       // per-family timings (record_timings)
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
     std::vector<int> leaves;  // per slab: tree leaves the last sweep wrote (fused stage 1)
+    bool csr = false;         // matrix-explicit backend (standard loop on CSR + tridiagonals)
     std::chrono::steady_clock::time_point t0;
+    double setup_s = 0.0;
     ~acg_solver() {
         for (acg_field* fl : {u, r, z, p, q})
             if (fl) free_field(fl);
@@ -1554,11 +1656,12 @@ void validate(const acg_solver_config* cfg) {
     if (cfg->variant == ACG_VARIANT_INTERLEAVED && cfg->backend == ACG_BACKEND_CSR)
         fail(ACG_ERR_INVALID_ARGUMENT,
              "SolverConfig: the interleaved variant exists for the matrix-free backend only");
-    if (cfg->backend == ACG_BACKEND_CSR)
-        fail(ACG_ERR_INVALID_ARGUMENT,
-             "SolverConfig: the CSR backend is not part of the B200 build (matrix-free only)");
+    if (cfg->backend != ACG_BACKEND_MATRIX_FREE && cfg->backend != ACG_BACKEND_CSR)
+        fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: unknown backend");
     if (cfg->variant != ACG_VARIANT_STANDARD && cfg->variant != ACG_VARIANT_INTERLEAVED)
         fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: unknown variant");
+    if (cfg->layout != ACG_LAYOUT_VERTICAL && cfg->layout != ACG_LAYOUT_HORIZONTAL)
+        fail(ACG_ERR_INVALID_ARGUMENT, "SolverConfig: unknown layout");
 }
 
 template <typename T>
@@ -1616,6 +1719,15 @@ void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
     s->t0 = std::chrono::steady_clock::now();
     s->launches0 = g_launches.load();
     s->f = f;
+    s->csr = s->cfg.backend == ACG_BACKEND_CSR;
+    if (s->csr) {  // make_backend (solver.hpp:147-154): assembly counts as setup
+        const auto t = std::chrono::steady_clock::now();
+        ensure_csr<T>(c, s->cfg.layout);
+        CK(cudaStreamSynchronize(c->stream));
+        s->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+    } else {
+        s->setup_s = 0.0;
+    }
     for (int a = 0; a < 4; ++a) {
         s->hv[a].clear();
         s->drained[a] = 0;
@@ -1647,7 +1759,10 @@ void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
     op_copy<T>(c, f, s->r, nullptr);
     // q = A u; r = r - q; ||r0||  (:295-305)
     s->timer.begin(kSpmv);
-    op_apply<T>(c, s->u, s->q, S[0]);
+    if (s->csr)
+        op_spmv_csr<T>(c, s->u, s->q, S[0]);
+    else
+        op_apply<T>(c, s->u, s->q, S[0]);
     s->timer.end(kSpmv);
     s->timer.begin(kBlas);
     op_axpy<T>(c, T(-1), nullptr, -1, false, s->q, s->r, false);
@@ -1655,7 +1770,10 @@ void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
     s->timer.end(kBlas);
     // z = M^-1 r; kappa_old = <r,z>  (:313-323)
     s->timer.begin(kPrec);
-    op_precondition<T>(c, s->r, s->z, S, S[0]);
+    if (s->csr)
+        op_tridiag<T>(c, s->r, s->z, S, S[0]);
+    else
+        op_precondition<T>(c, s->r, s->z, S, S[0]);
     s->timer.end(kPrec);
     s->timer.begin(kBlas);
     op_dot<T>(c, s->r, s->z, kOpKappa0, S, true);
@@ -1790,7 +1908,10 @@ void iterate_standard(acg_solver* s) {
     const acg_context* c = s->ctx;
     auto S = sv<T>(s);
     s->timer.begin(kSpmv);
-    op_apply<T>(c, s->p, s->q, S[0]);
+    if (s->csr)
+        op_spmv_csr<T>(c, s->p, s->q, S[0]);
+    else
+        op_apply<T>(c, s->p, s->q, S[0]);
     s->timer.end(kSpmv);
     s->timer.begin(kBlas);
     op_dot<T>(c, s->p, s->q, kOpStdSigma, S, true);
@@ -1799,7 +1920,10 @@ void iterate_standard(acg_solver* s) {
     op_dot<T>(c, s->r, s->r, kOpStdRnorm, S, true);
     s->timer.end(kBlas);
     s->timer.begin(kPrec);
-    op_precondition<T>(c, s->r, s->z, S, S[0]);
+    if (s->csr)
+        op_tridiag<T>(c, s->r, s->z, S, S[0]);
+    else
+        op_precondition<T>(c, s->r, s->z, S, S[0]);
     s->timer.end(kPrec);
     s->timer.begin(kBlas);
     op_dot<T>(c, s->r, s->z, kOpStdKappa, S, true);
@@ -1905,6 +2029,8 @@ void solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, doubl
                      "interleaved_prec_kernel: zero pivot in tridiagonal elimination");
             case kErrPivotPrecond:
                 fail(ACG_ERR_BREAKDOWN, "precondition: zero pivot in tridiagonal elimination");
+            case kErrPivotTridiag:
+                fail(ACG_ERR_BREAKDOWN, "solve_tridiag_set: zero pivot in tridiagonal elimination");
             case kErrKappa:
                 fail(ACG_ERR_BREAKDOWN, "%s: <r,z> not positive (preconditioner not SPD?)", var);
             default:
@@ -1918,7 +2044,8 @@ void solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, doubl
         s->timer.end(kBlas);
     }
     const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - s->t0).count();
-    T tr = op_true_residual<T>(c, s->u, s->f);
+    // residual_norm of the backend (solver.hpp:119-121 / :138-140)
+    T tr = s->csr ? op_true_residual_csr<T>(c, s->u, s->f, s->q) : op_true_residual<T>(c, s->u, s->f);
     if (u_out) op_copy<T>(c, s->u, u_out, nullptr);
     if (res) {
         std::memset(res, 0, sizeof(*res));
@@ -1930,6 +2057,7 @@ void solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, doubl
         res->n_alpha = h.n_alp;
         res->n_beta = h.n_bet;
         res->timings.total = total;
+        res->timings.setup = s->setup_s;
         if (s->timer.on) {
             CK(cudaStreamSynchronize(c->stream));
             res->timings.spmv = s->timer.seconds(kSpmv);
@@ -2125,10 +2253,12 @@ acg_status acg_solve_host(const acg_context* c, acg_layout layout, const void* f
         DeviceGuard g(c->device);
         CtxLock lk(c);
         PoolField ff(c), fu0(c), fu(c);
+        acg_solver_config cl = *cfg;
+        cl.layout = layout;  // CsrBackend orders its rows by the fields' layout (solver.hpp:129)
         ACG_TDISPATCH(c, {
             upload_t<T>(ff.f, f, layout, ACG_HOST_FULL);
             if (u0) upload_t<T>(fu0.f, u0, layout, ACG_HOST_FULL);
-            acg_solver* s = cached_solver<T>(c, cfg);
+            acg_solver* s = cached_solver<T>(c, &cl);
             solver_start<T>(s, ff.f, u0 ? fu0.f : nullptr);
             solver_run<T>(s);
             solver_finish<T>(s, fu.f, res, hr, hk, ha, hb);

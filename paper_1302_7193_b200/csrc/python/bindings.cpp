@@ -16,6 +16,7 @@
 #include <string>
 
 #include "acg.h"
+#include "anisocg/csr.hpp"
 #include "anisocg/field.hpp"
 #include "anisocg/grid.hpp"
 #include "anisocg/io.hpp"
@@ -103,45 +104,15 @@ std::pair<int, int> cost(const std::string& kernel, const std::string& cache) {
     return {flops[ki], mem[ki][ci]};
 }
 
-// Matrix-explicit stencil rows in vertical order (verification utility for
-// the reference's scipy cross-check; the GPU path never assembles a matrix).
-py::tuple assemble_csr(const OperatorContext<double>& ctx) {
-    const int m = ctx.m(), n_z = ctx.n_z();
-    const std::int64_t n = static_cast<std::int64_t>(ctx.n());
-    std::vector<std::int64_t> rp(n + 1, 0);
-    std::vector<std::int32_t> ci;
-    std::vector<double> va;
-    ci.reserve(n * 7);
-    va.reserve(n * 7);
-    for (int i = 0; i < m; ++i)
-        for (int j = 0; j < m; ++j)
-            for (int k = 0; k < n_z; ++k) {
-                const std::int64_t l = (static_cast<std::int64_t>(i) * m + j) * n_z + k;
-                const double A = ctx.area(i, j), dk = ctx.d()[k];
-                std::array<std::pair<std::int64_t, double>, 7> e;
-                int c = 0;
-                auto idx = [&](int a, int b, int kk) {
-                    return (static_cast<std::int64_t>(a) * m + b) * n_z + kk;
-                };
-                if (i > 0) e[c++] = {idx(i - 1, j, k), ctx.alpha_east(i - 1, j) * dk};
-                if (j > 0) e[c++] = {idx(i, j - 1, k), ctx.alpha_north(i, j - 1) * dk};
-                if (k > 0) e[c++] = {idx(i, j, k - 1), A * ctx.c_prime()[k] * dk};
-                e[c++] = {l, ((ctx.a_prime()[k] - ctx.b_prime()[k] - ctx.c_prime()[k]) * A -
-                              ctx.alpha_diag(i, j)) * dk};
-                if (k + 1 < n_z) e[c++] = {idx(i, j, k + 1), A * ctx.b_prime()[k] * dk};
-                if (j + 1 < m) e[c++] = {idx(i, j + 1, k), ctx.alpha_north(i, j) * dk};
-                if (i + 1 < m) e[c++] = {idx(i + 1, j, k), ctx.alpha_east(i, j) * dk};
-                for (int a = 0; a < c; ++a) {
-                    ci.push_back(static_cast<std::int32_t>(e[a].first));
-                    va.push_back(e[a].second);
-                }
-                rp[l + 1] = static_cast<std::int64_t>(va.size());
-            }
-    py::array_t<std::int64_t> a(static_cast<py::ssize_t>(rp.size()));
-    std::memcpy(a.mutable_data(), rp.data(), rp.size() * sizeof(std::int64_t));
-    py::array_t<std::int32_t> b(static_cast<py::ssize_t>(ci.size()));
-    std::memcpy(b.mutable_data(), ci.data(), ci.size() * sizeof(std::int32_t));
-    return py::make_tuple(a, b, vec(va));
+// assemble_csr(ctx, VerticalContiguous) as (row_ptr, col_idx, vals) arrays
+// (bindings.cpp:179-193; host utility for the scipy cross-check).
+py::tuple csr_arrays(const OperatorContext<double>& ctx) {
+    const CsrMatrix<double> A = assemble_csr(ctx, Layout::VerticalContiguous);
+    py::array_t<std::int64_t> a(static_cast<py::ssize_t>(A.row_ptr.size()));
+    std::memcpy(a.mutable_data(), A.row_ptr.data(), A.row_ptr.size() * sizeof(std::int64_t));
+    py::array_t<std::int32_t> b(static_cast<py::ssize_t>(A.col_idx.size()));
+    std::memcpy(b.mutable_data(), A.col_idx.data(), A.col_idx.size() * sizeof(std::int32_t));
+    return py::make_tuple(a, b, vec(A.vals));
 }
 
 template <typename T, typename Cls>
@@ -406,7 +377,7 @@ PYBIND11_MODULE(_anisocg, mod) {
     bind_ops<double>(mod);
     bind_blas<double>(mod);
 
-    mod.def("assemble_csr", &assemble_csr, py::arg("ctx"),
+    mod.def("assemble_csr", &csr_arrays, py::arg("ctx"),
             "CSR arrays (row_ptr, col_idx, vals) in vertically contiguous row order "
             "(host verification utility)");
     mod.def(

