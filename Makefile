@@ -22,8 +22,13 @@ HOSTSRC := $(CSRC)/host/grid.cpp $(CSRC)/host/profile.cpp $(CSRC)/host/shim.cpp 
            $(CSRC)/host/cost_model.cpp $(CSRC)/host/io.cpp
 HDRS    := include/acg.h $(wildcard include/anisocg/*.hpp) $(CSRC)/acg_internal.h
 
-.PHONY: all lib py oracle clean
-all: lib py oracle
+.PHONY: all lib py oracle micro clean
+all: lib py oracle micro
+
+# sanitizer evidence kernel (tests/test_sanitizers.py)
+micro: scripts/micro/tmem_synccheck
+scripts/micro/tmem_synccheck: scripts/micro/tmem_synccheck.cu
+	$(NVCC) $(ARCH) -o $@ $<
 
 lib: $(LIB)
 py: $(PYMOD)

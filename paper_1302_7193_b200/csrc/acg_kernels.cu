@@ -18,8 +18,6 @@
 // order (the reference builds with -ffp-contract=off), which makes the GPU
 // bit-identical to the CPU. The FAST path allows FMA contraction and replaces
 // the three divides per Thomas level by one reciprocal.
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -271,158 +269,10 @@ __device__ void cta_finish(const FinishDev<T>& fin, const T* stage, int nleaves,
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
 #include "acg_thomas_tm.cuh"
-#include "acg_thomas_tma.cuh"
 #include "acg_thomas_tm2.cuh"
 
 // ================================================================ K2 / K3 / K8
 constexpr int kStencilWarps = 8;
-
-// K2: u += a p; p = z + b p; q = A z + b q; sigma partial (operator.hpp:243-261)
-template <typename T, bool Fast>
-__global__ void __launch_bounds__(32 * kStencilWarps)
-    k_fused_spmv(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p, T* __restrict__ q,
-                 const T* __restrict__ z, T* __restrict__ part, const Scalars<T>* __restrict__ S) {
-    using A = Ar<T, Fast>;
-    if (S->done) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* prof = reinterpret_cast<T*>(smem_raw);
-    const int n_z = v.n_z, m = v.m;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    load_profile(prof, v.prof, 4 * n_z, tid, 32 * kStencilWarps);
-    __syncthreads();
-    const int j = blockIdx.x * 32 + threadIdx.x;
-    const int il = blockIdx.y * kStencilWarps + threadIdx.y;
-    if (j >= m || il >= v.m_loc) return;
-    const T* sP = prof + kProfS * n_z;
-    const T* bP = prof + kProfB * n_z;
-    const T* cP = prof + kProfC * n_z;
-    const T* dP = prof + kProfD * n_z;
-    const Col<T> c = load_col(v, il, j);
-    const T alpha = S->alpha, beta = S->beta;
-    const long long base = static_cast<long long>(il) * v.plane + j;
-    const T* zc = z + base;
-    T* uc = u + base;
-    T* pc = p + base;
-    T* qc = q + base;
-    T z0 = zc[0], zd = z0, sig = T(0);
-#pragma unroll 4
-    for (int k = 0; k < n_z; ++k) {
-        const long long l = static_cast<long long>(k) * m;
-        const T zu = (k + 1 < n_z) ? zc[l + m] : z0;
-        const T ze = zc[l + c.oe], zw = zc[l + c.ow], zn = zc[l + c.on], zs = zc[l + c.os];
-        T ps = __ldcs(pc + l), qs = __ldcs(qc + l);
-        const T uv = __ldcs(uc + l);
-        __stcs(uc + l, A::add(uv, A::mul(alpha, ps)));
-        ps = A::add(A::mul(beta, ps), z0);
-        qs = A::mul(beta, qs);
-        __stcs(pc + l, ps);
-        const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an,
-                                      c.as, z0, zu, zd, ze, zw, zn, zs);
-        qs = A::add(qs, A::mul(dP[k], dq));
-        sig = A::add(sig, A::mul(ps, qs));
-        __stcs(qc + l, qs);
-        zd = z0;
-        z0 = zu;
-    }
-    part[static_cast<long long>(il) * m + j] = sig;
-}
-
-// K2 with a cp.async ring: p, q, u and the next level of z are copied D levels
-// ahead into a per-thread shared-memory ring (asynchronous, no registers held),
-// so each SM keeps ~(warps x 32 x D x 32 B) in flight; the four horizontal z
-// neighbours are plain loads that hit L1/L2 (the rows belong to adjacent warps).
-constexpr int kSpmvD = 6;
-
-// X: warps of a CTA along j (X = 1: 8 i-planes x 32 j; X = 8: 1 plane x 256 j).
-template <typename T, bool Fast, int X = 1, int D = kSpmvD, int MINB = 1>
-__global__ void __launch_bounds__(32 * kStencilWarps, MINB)
-    k_fused_spmv_ring(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
-                      T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
-    using A = Ar<T, Fast>;
-    constexpr int NT = 32 * kStencilWarps, NS = D + 1;
-    if (S->done) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* prof = reinterpret_cast<T*>(smem_raw);
-    const int n_z = v.n_z, m = v.m;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    load_profile(prof, v.prof, 4 * n_z, tid, NT);
-    __syncthreads();
-    const int j = (blockIdx.x * X + threadIdx.y % X) * 32 + threadIdx.x;
-    const int il = blockIdx.y * (kStencilWarps / X) + threadIdx.y / X;
-    if (j >= m || il >= v.m_loc) return;
-    T* ring = prof + 4 * n_z;
-    const T* sP = prof + kProfS * n_z;
-    const T* bP = prof + kProfB * n_z;
-    const T* cP = prof + kProfC * n_z;
-    const T* dP = prof + kProfD * n_z;
-    const Col<T> c = load_col(v, il, j);
-    const T alpha = S->alpha, beta = S->beta;
-    const long long base = static_cast<long long>(il) * v.plane + j;
-    const T* zc = z + base;
-    T* uc = u + base;
-    T* pc = p + base;
-    T* qc = q + base;
-    auto slot = [&](int s, int a) -> T* { return ring + (s * 4 + a) * NT + tid; };
-    auto issue = [&](int k, int s) {
-        const long long l = static_cast<long long>(k) * m;
-        cpa(slot(s, 0), pc + l);
-        cpa(slot(s, 1), qc + l);
-        cpa(slot(s, 2), uc + l);
-        if (k + 1 < n_z) cpa(slot(s, 3), zc + l + m);
-    };
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        if (t < n_z) issue(t, t);
-        cp_commit();
-    }
-    int cs = 0, ps_ = D;
-    T z0 = zc[0], zd = z0, sig = T(0);
-    // horizontal neighbours are loaded one level ahead (their L1/L2 latency then
-    // overlaps a whole level of work instead of stalling it)
-    T ze = zc[c.oe], zw = zc[c.ow], zn = zc[c.on], zs = zc[c.os];
-    for (int k = 0; k < n_z; ++k) {
-        const long long l = static_cast<long long>(k) * m;
-        const T ce = ze, cw = zw, cn = zn, cs_ = zs;
-        if (k + 1 < n_z) {
-            const long long l1 = l + m;
-            ze = zc[l1 + c.oe];
-            zw = zc[l1 + c.ow];
-            zn = zc[l1 + c.on];
-            zs = zc[l1 + c.os];
-        }
-        cp_wait<D - 1>();
-        T pv = *slot(cs, 0), qv = *slot(cs, 1);
-        const T uv = *slot(cs, 2);
-        const T zu = (k + 1 < n_z) ? *slot(cs, 3) : z0;
-        if (k + D < n_z) issue(k + D, ps_);
-        cp_commit();
-        cs = cs + 1 == NS ? 0 : cs + 1;
-        ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
-        __stcs(uc + l, A::add(uv, A::mul(alpha, pv)));
-        pv = A::add(A::mul(beta, pv), z0);
-        qv = A::mul(beta, qv);
-        __stcs(pc + l, pv);
-        const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw, c.an, c.as,
-                                      z0, zu, zd, ce, cw, cn, cs_);
-        qv = A::add(qv, A::mul(dP[k], dq));
-        sig = A::add(sig, A::mul(pv, qv));
-        __stcs(qc + l, qv);
-        zd = z0;
-        z0 = zu;
-    }
-    cp_wait<0>();
-    if (stage != nullptr) {  // fused reduction stage 1 (X = 8: one plane x 256 j, all valid)
-        __syncthreads();
-        ring[tid] = sig;
-        __syncthreads();
-        if (threadIdx.y == 0)
-            cta_subtree_sums<T, NT>(ring, 1, stage, nleaves,
-                                    (static_cast<long long>(il) * m + blockIdx.x * NT) / NT);
-        return;
-    }
-    part[static_cast<long long>(il) * m + j] = sig;
-}
 
 // K3: y = A x (operator.hpp:124-133)
 template <typename T, bool Fast>
@@ -1106,9 +956,8 @@ void ensure_smem(KernelT kernel, size_t bytes) {
 }
 
 
-// Thomas launch configuration (warps per block, phi checkpoint stride, cp.async
-// depth), chosen per precision; ACG_THOMAS_OCC pads shared memory to cap the
-// resident blocks per SM (L2-footprint experiments).
+// Thomas launch configuration of the global-memory fallback k_thomas (warps per
+// block, phi checkpoint stride, cp.async depth), per precision.
 using ThomasF64 = ThomasCfg<4, 4, 7>;
 using ThomasF32 = ThomasCfg<4, 2, 7>;
 template <typename T>
@@ -1118,56 +967,21 @@ struct ThomasOf<double> { using type = ThomasF64; };
 template <>
 struct ThomasOf<float> { using type = ThomasF32; };
 
-// ACG_L2_HINTS=0 disables the L2 eviction-priority hints (A/B experiments).
-inline int l2_hints() {
-    static int h = [] {
-        const char* e = std::getenv("ACG_L2_HINTS");
-        return e ? std::atoi(e) : 0;
-    }();
-    return h;
-}
-
-inline size_t thomas_pad(size_t bytes) {
-    static int occ = [] {
-        const char* e = std::getenv("ACG_THOMAS_OCC");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (occ > 0) {
-        const size_t want = (227u * 1024u) / static_cast<size_t>(occ) - 1024u;
-        if (want > bytes) return want;
-    }
-    return bytes;
-}
-
 template <typename T, bool Fast, bool Fused, class C>
 void launch_thomas_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
                        Scalars<T>* S, const Scalars<T>* gate, T* phi_scratch, cudaStream_t st) {
     const dim3 block(32, C::W);
     const dim3 grid((v.m + 31) / 32, (v.m_loc + C::W - 1) / C::W);
-    const size_t smem = thomas_pad(thomas_smem_bytes<T, C>(v.n_z, phi_scratch != nullptr));
+    const size_t smem = thomas_smem_bytes<T, C>(v.n_z, phi_scratch != nullptr);
     if (phi_scratch) {
         ensure_smem(k_thomas<T, Fast, Fused, C, true>, smem);
         k_thomas<T, Fast, Fused, C, true>
-            <<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch, l2_hints());
+            <<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch);
     } else {
         ensure_smem(k_thomas<T, Fast, Fused, C, false>, smem);
         k_thomas<T, Fast, Fused, C, false>
-            <<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch, l2_hints());
+            <<<grid, block, smem, st>>>(v, r, in, out, p2, pk, S, gate, phi_scratch);
     }
-}
-
-// ACG_THOMAS="W,CP,D" selects one of the compiled configurations (tuning sweeps).
-inline int thomas_choice() {
-    static int c = [] {
-        const char* e = std::getenv("ACG_THOMAS");
-        if (!e) return 0;
-        const std::string s(e);
-        const char* names[] = {"", "2,4,7", "4,4,7"};
-        for (int a = 1; a < 3; ++a)
-            if (s == names[a]) return a;
-        return 0;
-    }();
-    return c;
 }
 
 // Leaves of the reduction tree a sweep can emit directly (cta_subtree_sums):
@@ -1187,11 +1001,7 @@ inline int num_sms() {
 
 template <typename T>
 int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
-    static const bool off = [] {
-        const char* e = std::getenv("ACG_FUSED_REDUCE");
-        return e && std::string(e) == "0";
-    }();
-    if (off || stage == nullptr || cols <= 0 || v.m % cols != 0) return 0;
+    if (stage == nullptr || cols <= 0 || v.m % cols != 0) return 0;
     const long long ncol = static_cast<long long>(v.m_loc) * v.m;
     if ((ncol & (ncol - 1)) != 0 || ncol / cols > kMaxFusedLeaves || ncol / cols < 1) return 0;
     return static_cast<int>(ncol / cols);
@@ -1211,36 +1021,22 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     // consecutive planes. The largest tpc <= 4 that keeps >= 6 waves of the 2
     // resident CTAs per SM with a last wave >= 97% full (C3: 4, K1 0.789 ->
     // 0.777 ms; tpc 3, 5, 6 leave a 24-62% last wave: 0.80-0.81 ms; 8: 0.855 ms).
-    // ACG_TM_TPC=n overrides.
-    static const int tpc_env = [] {
-        const char* e = std::getenv("ACG_TM_TPC");
-        return e ? std::max(1, std::atoi(e)) : 0;
-    }();
     int tpc = 1;
     if (C::X == 4 && !v.halo.on && fin == nullptr) {
-        if (tpc_env) {
-            tpc = tpc_env;
-        } else {
-            const double slots = 2.0 * num_sms();
-            const long long rows = (v.m + 127) / 128;
-            for (int t = 4; t > 1; --t) {
-                const double waves = static_cast<double>(rows * ((v.m_loc + t - 1) / t)) / slots;
-                if (waves >= 6.0 && waves / std::ceil(waves) >= 0.97) {
-                    tpc = t;
-                    break;
-                }
+        const double slots = 2.0 * num_sms();
+        const long long rows = (v.m + 127) / 128;
+        for (int t = 4; t > 1; --t) {
+            const double waves = static_cast<double>(rows * ((v.m_loc + t - 1) / t)) / slots;
+            if (waves >= 6.0 && waves / std::ceil(waves) >= 0.97) {
+                tpc = t;
+                break;
             }
         }
     }
     const dim3 grid((v.m + 32 * C::X - 1) / (32 * C::X),
                     C::X == 4 ? (v.m_loc + tpc - 1) / tpc : (v.m_loc + PW - 1) / PW);
     size_t smem = thomas_tm_smem_bytes<T, C>(v.n_z);
-    static const size_t occ_cap = [] {  // ACG_TM_OCC=n caps resident CTAs per SM (experiments)
-        const char* e = std::getenv("ACG_TM_OCC");
-        return static_cast<size_t>(e ? std::atoi(e) : 0);
-    }();
-    size_t max_ctas = 512u / tcols;
-    if (occ_cap > 0 && occ_cap < max_ctas) max_ctas = occ_cap;
+    const size_t max_ctas = 512u / tcols;
     const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
     if (smem < floor_bytes) smem = floor_bytes;
     // fused stage 1: CTA = one aligned node (128 consecutive columns) of the tree
@@ -1258,61 +1054,6 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
                tpc);
     return leaves;
 }
-
-// 2D TMA view of a plane-major field: dim0 = j (m), dim1 = row = plane*n_z + k
-// over the slab's m_loc planes plus its two ghost planes; box = 8 levels x box_j.
-// `data` points at plane 0 (the ghost plane precedes it). false if the driver
-// entry point is unavailable or the rows are not 16-byte aligned.
-template <typename T>
-bool make_field_map(CUtensorMap* map, const SlabView<T>& v, const T* data, int box_j) {
-    static PFN_cuTensorMapEncodeTiled encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-                cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            fn = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
-    }();
-    if (!encode || (static_cast<size_t>(v.m) * sizeof(T)) % 16 != 0) return false;
-    const T* base = data - v.plane;
-    if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(v.m),
-                                static_cast<cuuint64_t>(v.m_loc + 2) * v.n_z};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(v.m) * sizeof(T)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_j), 8};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
-                                                  : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                              2, const_cast<T*>(base), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-// TMA-fed TMEM sweep (k_thomas_tma); returns -1 when the tensor maps cannot be
-// built (the caller then uses k_thomas_tm).
-template <typename T, bool Fast, bool Fused, class C>
-int launch_thomas_tma_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
-                          Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
-    CUtensorMap m0, m1;
-    if (!make_field_map<T>(&m0, v, Fused ? r : in, 32)) return -1;
-    if (Fused && !make_field_map<T>(&m1, v, in, 32)) return -1;
-    if (!Fused) m1 = m0;
-    const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
-    const dim3 block(32, C::W);
-    const dim3 grid((v.m + C::NT - 1) / C::NT, v.m_loc);
-    size_t smem = thomas_tma_smem_bytes<T, C>(v.n_z);
-    const size_t max_ctas = 512u / tcols;
-    const size_t floor_bytes = 233472u / (max_ctas + 1) - 1024u + 64u;
-    if (smem < floor_bytes) smem = floor_bytes;
-    const int leaves = fused_leaves(v, C::NT, Fused ? stage : nullptr);
-    ensure_smem(k_thomas_tma<T, Fast, Fused, C>, smem);
-    k_thomas_tma<T, Fast, Fused, C><<<grid, block, smem, st>>>(
-        v, m0, m1, r, in, out, p2, pk, S, gate, tcols, leaves ? stage : nullptr, leaves);
-    return leaves;
-}
-
 
 // Two columns per thread, persistent (k_thomas_tm2); -1 if not applicable.
 template <typename T, bool Fast, bool Fused, class C>
@@ -1334,95 +1075,38 @@ int launch_thomas_tm2_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
     return leaves;
 }
 
-// Two columns per thread: default for fp32 (C4: K1 1.51 vs 2.09 ms, the fp32
-// sweep moves half the bytes per instruction), off for fp64 (C3: 0.99 vs
-// 0.80 ms). ACG_THOMAS_TM2=0/1 overrides.
-template <typename T>
-int thomas_tm2_choice() {
-    static int c = [] {
-        const char* e = std::getenv("ACG_THOMAS_TM2");
-        if (e) return std::string(e) == "1" ? 1 : 0;
-        return sizeof(T) == 4 ? 1 : 0;
-    }();
-    return c;
-}
-
-inline bool thomas_tma_enabled() {  // ACG_THOMAS_TMA=1 opts in (measured: no faster than k_thomas_tm)
-    static bool on = [] {
-        const char* e = std::getenv("ACG_THOMAS_TMA");
-        return e && std::string(e) == "1";
-    }();
-    return on;
-}
-
-// ACG_THOMAS_TM="CP,D,DB" selects a compiled TMEM configuration; "0" disables
-// the TMEM sweep (A/B experiments).
-inline int thomas_tm_choice() {
-    static int c = [] {
-        const char* e = std::getenv("ACG_THOMAS_TM");
-        if (!e) return 1;
-        const std::string s(e);
-        const char* names[] = {"0", "4,15,15", "4,15,15,1", "8,15,15", "2,15,15", "q1", "q8", "q4", "q8b"};
-        for (int a = 0; a < 9; ++a)
-            if (s == names[a]) return a;
-        return 1;
-    }();
-    return c;
-}
+// K1/K4 kernel choice (measured):
+//  * fp32: k_thomas_tm2, two columns per thread with both z' columns in TMEM
+//    (C4: K1 1.51 vs 2.09 ms for one column per thread — the fp32 sweep moves
+//    half the bytes per instruction); needs even m;
+//  * fp64, and fp32 with odd m: k_thomas_tm, one column per thread, z' in TMEM
+//    (C3: 0.78 ms; two columns per thread 0.99 ms);
+//  * k_thomas (z' through global memory) when the TMEM sweep cannot run: n_z*s
+//    above 1 KiB, or division operand ranges that fail k_validate_tm.
+// Measured-slower configurations (TMA-fed tiles, other ring depths and CTA
+// shapes, occupancy caps) were removed after round 1; DESIGN.md keeps their numbers.
+using ThomasTmDefault = ThomasTmCfg<4, 15, 15>;
+using ThomasTm2Default = ThomasTm2Cfg<4, 15, 15>;
 
 template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
                   const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st,
                   Finish<T>* fin = nullptr) {
-    const int tmc = thomas_tm_choice();
-    const int tm2 = thomas_tm2_choice<T>();
-    if (v.halo.on) {  // fused halo (fused_halo_ok): a TMEM sweep that carries the planes
-        if (tmc != 0 && v.tm_ok && phi_scratch == nullptr) {
-            if (tm2 != 0) {
-                const int l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Cfg<4, 15, 15>>(
-                    v, r, in, out, p2, pk, S, gate, stage, st);
-                if (l >= 0) return l;
-            }
-            if (thomas_tm_cols(v.n_z, sizeof(T)) <= 256)
-                return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmCfg<4, 15, 15>>(
-                    v, r, in, out, p2, pk, S, gate, stage, st, fin);
-        }
+    const bool tmem = v.tm_ok && phi_scratch == nullptr;
+    if (tmem && sizeof(T) == 4) {
+        const int l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Default>(v, r, in, out, p2, pk,
+                                                                             S, gate, stage, st);
+        if (l >= 0) return l;
+    }
+    if (tmem && thomas_tm_cols(v.n_z, sizeof(T)) <= 256)
+        return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmDefault>(v, r, in, out, p2, pk, S, gate,
+                                                                    stage, st, fin);
+    if (v.halo.on) {  // fused_halo_ok admits only the TMEM sweeps
         std::fprintf(stderr, "acg: fused halo requested for a sweep that cannot carry it\n");
         std::abort();
     }
-    if (tm2 != 0 && tmc != 0 && v.tm_ok && phi_scratch == nullptr && !thomas_tma_enabled()) {
-        int l = -1;
-        l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Cfg<4, 15, 15>>(v, r, in, out, p2, pk, S,
-                                                                        gate, stage, st);
-        if (l >= 0) return l;
-    }
-    if (thomas_tma_enabled() && tmc != 0 && v.tm_ok && phi_scratch == nullptr &&
-        thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
-        const int l = launch_thomas_tma_cfg<T, Fast, Fused, ThomasTmaCfg<4, 3>>(v, r, in, out, p2, pk,
-                                                                               S, gate, stage, st);
-        if (l >= 0) return l;
-    }
-    if (tmc != 0 && v.tm_ok && phi_scratch == nullptr && thomas_tm_cols(v.n_z, sizeof(T)) <= 256) {
-#define ACG_TM(...) return launch_thomas_tm_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, stage, st, fin)
-        switch (tmc) {
-            case 2: ACG_TM(ThomasTmCfg<4, 15, 15, 1>);
-            case 3: ACG_TM(ThomasTmCfg<8, 15, 15>);
-            case 4: ACG_TM(ThomasTmCfg<2, 15, 15>);
-            case 5: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 1>);
-            case 6: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 8>);
-            case 7: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 4>);
-            case 8: ACG_TM(ThomasTmCfg<4, 15, 15, 4, 8>);
-            default: ACG_TM(ThomasTmCfg<4, 15, 15>);
-        }
-#undef ACG_TM
-    }
-#define ACG_TH(...) launch_thomas_cfg<T, Fast, Fused, __VA_ARGS__>(v, r, in, out, p2, pk, S, gate, phi_scratch, st)
-    switch (thomas_choice()) {
-        case 1: ACG_TH(ThomasCfg<2, 4, 7>); break;
-        case 2: ACG_TH(ThomasCfg<4, 4, 7>); break;
-        default: ACG_TH(typename ThomasOf<T>::type); break;
-    }
-#undef ACG_TH
+    launch_thomas_cfg<T, Fast, Fused, typename ThomasOf<T>::type>(v, r, in, out, p2, pk, S, gate,
+                                                                  phi_scratch, st);
     return 0;
 }
 
@@ -1487,23 +1171,13 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
     post_launch("precondition");
 }
 
-// K2 variant: ACG_SPMV=plain|ring|tile|pair|pair2 overrides; default: the
-// two-column kernels (the tile kernel for odd m) — fp64 with every stencil
-// input in the cp.async ring (C3 K2 1.18 ms), fp32 with the neighbour rows
-// loaded a level ahead (C4 K2 2.59 ms); measured.
-template <typename T>
-int spmv_mode() {
-    static const int mode = [] {
-        const char* e = std::getenv("ACG_SPMV");
-        if (e && std::string(e) == "plain") return 1;
-        if (e && std::string(e) == "ring") return 2;
-        if (e && std::string(e) == "tile") return 0;
-        if (e && std::string(e) == "pair") return 5;
-        if (e && std::string(e) == "pair2") return 6;
-        return sizeof(T) == 4 ? 5 : 6;
-    }();
-    return mode;
-}
+// K2 kernel choice (measured): two adjacent columns per thread
+// for even m — fp64 k_fused_spmv_pair2 (every stencil input in a 3-level
+// cp.async ring, C3 K2 1.18 ms), fp32 k_fused_spmv_pair (neighbour rows loaded
+// a level ahead, C4 K2 2.49 ms); k_fused_spmv_tile (shared z tiles) for odd m.
+// Measured-slower kernels (one column per thread with plain or ring loads) and
+// the other ring depths were removed after round 1.
+inline bool spmv_pairs(int m) { return m % 2 == 0; }
 
 template <typename T>
 bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
@@ -1512,20 +1186,17 @@ bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
         const char* e = std::getenv("ACG_FUSED_HALO");
         return e && std::string(e) == "0";
     }();
-    // producer: k_thomas_tm2 (fp32 default) or k_thomas_tm (default configuration);
-    // consumer: k_fused_spmv_pair (fp32 default) or k_fused_spmv_pair2 (fp64 default)
+    // producer: k_thomas_tm2 (fp32) or k_thomas_tm (fp64); consumer: k_fused_spmv_pair
+    // (fp32) or k_fused_spmv_pair2 (fp64)
     const unsigned cols = thomas_tm_cols(v.n_z, sizeof(T));
-    const bool k1 = (thomas_tm2_choice<T>() != 0 && 2 * cols <= 512) || cols <= 256;
-    const int mode = spmv_mode<T>();
-    return !off && thomas_tm_choice() != 0 && v.tm_ok && !phi_in_hbm && k1 &&
-           (mode == 5 || mode == 6) && v.m % 2 == 0;
+    const bool k1 = sizeof(T) == 4 ? 2 * cols <= 512 : cols <= 256;
+    return !off && v.tm_ok && !phi_in_hbm && k1 && spmv_pairs(v.m);
 }
 
 template <typename T>
 bool spmv_plane_ranges(const SlabView<T>& v, bool fast) {
     (void)fast;
-    const int mode = spmv_mode<T>();
-    return (mode == 5 || mode == 6) && v.m % 2 == 0;
+    return spmv_pairs(v.m);
 }
 
 template <typename T>
@@ -1533,151 +1204,63 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
                       const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin) {
     int leaves = 0;
     const dim3 block(32, kStencilWarps);
-    const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
-    const int mode = spmv_mode<T>();
-    if (v.halo.on && !((mode == 5 || mode == 6) && v.m % 2 == 0 && v.plane_count == 0)) {
+    if (v.halo.on && !(spmv_pairs(v.m) && v.plane_count == 0)) {
         std::fprintf(stderr, "acg: fused halo requested for a stencil sweep that cannot carry it\n");
         std::abort();
     }
-    static const int pair_cfg = [] {  // ACG_SPMV_PAIR = 10*D + min CTAs per SM
-        const char* e = std::getenv("ACG_SPMV_PAIR");
-        return e ? std::atoi(e) : (sizeof(T) == 4 ? 23 : 32);
-    }();
-    static const int tile_d = [] {
-        const char* e = std::getenv("ACG_SPMV_D");
-        return e ? std::atoi(e) : 5;
-    }();
-    if (mode == 1) {
-        const size_t smem = sizeof(T) * 4 * static_cast<size_t>(v.n_z);
-        if (fast) {
-            ensure_smem(k_fused_spmv<T, true>, smem);
-            k_fused_spmv<T, true><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+    if (spmv_pairs(v.m)) {
+        constexpr int kCols = 2 * 32 * kStencilWarps;  // columns per CTA (one i-plane)
+        leaves = fused_leaves(v, kCols, stage);
+        T* stg = leaves ? stage : nullptr;
+        const dim3 g2((v.m + kCols - 1) / kCols, v.plane_count ? v.plane_count : v.m_loc);
+        if (sizeof(T) == 4) {
+            // ring depth 2 (exact: at least 3 CTAs per SM)
+            constexpr int D = 2;
+            const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
+                                             static_cast<size_t>(D + 1) * 4 * kCols);
+            if (fast) {
+                ensure_smem(k_fused_spmv_pair<T, true, D, 2>, smem);
+                k_fused_spmv_pair<T, true, D, 2><<<g2, block, smem, st>>>(v, u, p, q, z, part, S,
+                                                                         stg, leaves);
+            } else {
+                ensure_smem(k_fused_spmv_pair<T, false, D, 3>, smem);
+                k_fused_spmv_pair<T, false, D, 3><<<g2, block, smem, st>>>(v, u, p, q, z, part, S,
+                                                                          stg, leaves);
+            }
         } else {
-            ensure_smem(k_fused_spmv<T, false>, smem);
-            k_fused_spmv<T, false><<<grid, block, smem, st>>>(v, u, p, q, z, part, S);
+            // ring depth 3, at least 2 CTAs per SM
+            constexpr int D = 3;
+            const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
+                                             static_cast<size_t>(D + 1) * 7 * kCols);
+            FinishDev<T> fd{nullptr, nullptr, -1};
+            if (fin && leaves > 0 &&
+                static_cast<size_t>(leaves) + 4 * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
+                fd = {fin->S, fin->counter, fin->op};
+                fin->used = true;
+            }
+            if (fast) {
+                ensure_smem(k_fused_spmv_pair2<T, true, D, 2>, smem);
+                launch_pdl(k_fused_spmv_pair2<T, true, D, 2>, g2, block, smem, st, v, u, p, q, z,
+                           part, S, stg, leaves, fd);
+            } else {
+                ensure_smem(k_fused_spmv_pair2<T, false, D, 2>, smem);
+                launch_pdl(k_fused_spmv_pair2<T, false, D, 2>, g2, block, smem, st, v, u, p, q, z,
+                           part, S, stg, leaves, fd);
+            }
         }
-    } else if (mode == 5 && v.m % 2 == 0) {
-        const int Dp = pair_cfg / 10;
-        leaves = fused_leaves(v, 2 * 32 * kStencilWarps, stage);
-        T* stg = leaves ? stage : nullptr;
-        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
-                                         static_cast<size_t>(Dp + 1) * 4 * 2 * 32 * kStencilWarps);
-        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps),
-                      v.plane_count ? v.plane_count : v.m_loc);
-#define ACG_PR(F, DD, MB)                                                                         \
-    do {                                                                                          \
-        ensure_smem(k_fused_spmv_pair<T, F, DD, MB>, smem);                                       \
-        k_fused_spmv_pair<T, F, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
-    } while (0)
-        switch (fast ? -pair_cfg : pair_cfg) {
-            case 22: ACG_PR(false, 2, 2); break;
-            case 32: ACG_PR(false, 3, 2); break;
-            case 42: ACG_PR(false, 4, 2); break;
-            case 23: ACG_PR(false, 2, 3); break;
-            case 33: ACG_PR(false, 3, 3); break;
-            case 24: ACG_PR(false, 2, 4); break;
-            case -22: ACG_PR(true, 2, 2); break;
-            case -33: ACG_PR(true, 3, 3); break;
-            default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
-        }
-#undef ACG_PR
-    } else if (mode == 6 && v.m % 2 == 0) {
-        const int Dp = pair_cfg / 10;
-        leaves = fused_leaves(v, 2 * 32 * kStencilWarps, stage);
-        T* stg = leaves ? stage : nullptr;
-        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
-                                         static_cast<size_t>(Dp + 1) * 7 * 2 * 32 * kStencilWarps);
-        const dim3 g2((v.m + 2 * 32 * kStencilWarps - 1) / (2 * 32 * kStencilWarps),
-                      v.plane_count ? v.plane_count : v.m_loc);
-        FinishDev<T> fd{nullptr, nullptr, -1};
-        if (fin && leaves > 0 &&
-            static_cast<size_t>(leaves) + 4 * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
-            fd = {fin->S, fin->counter, fin->op};
-            fin->used = true;
-        }
-#define ACG_PR(F, DD, MB)                                                                         \
-    do {                                                                                          \
-        ensure_smem(k_fused_spmv_pair2<T, F, DD, MB>, smem);                                      \
-        launch_pdl(k_fused_spmv_pair2<T, F, DD, MB>, g2, block, smem, st, v, u, p, q, z, part, S, stg, leaves, fd); \
-    } while (0)
-        switch (fast ? -pair_cfg : pair_cfg) {
-            case 22: ACG_PR(false, 2, 2); break;
-            case 32: ACG_PR(false, 3, 2); break;
-            case 23: ACG_PR(false, 2, 3); break;
-            case 13: ACG_PR(false, 1, 3); break;
-            case 41: ACG_PR(false, 4, 1); break;
-            case 51: ACG_PR(false, 5, 1); break;
-            case 31: ACG_PR(false, 3, 1); break;
-            case 33: ACG_PR(false, 3, 3); break;
-            case 43: ACG_PR(false, 4, 3); break;
-            case -32: ACG_PR(true, 3, 2); break;
-            default: if (fast) ACG_PR(true, 2, 2); else ACG_PR(false, 2, 2); break;
-        }
-#undef ACG_PR
-    } else if (mode == 2) {
-        // ring depth: D levels (or 10*D + min CTAs/SM); measured best at C3:
-        // D = 2 with 4 CTAs (32 warps) per SM, 1.28 vs 1.33 ms for D = 6 with 3
-        static const int Dr = [] {
-            const char* e = std::getenv("ACG_SPMV_D");
-            return e ? std::atoi(e) : 24;
-        }();
-        // X: warps along j, the widest contiguous row chunk m allows (env override)
-        static const int Xenv = [] {
-            const char* e = std::getenv("ACG_SPMV_X");
-            return e ? std::atoi(e) : 0;
-        }();
-        const int X = Xenv ? Xenv
-                           : (v.m % 256 == 0 ? 8 : v.m % 128 == 0 ? 4 : v.m % 64 == 0 ? 2 : 1);
-        // ring depth actually launched (must match the dispatch below)
-        const int Dx = X == 8 && (Dr == 24 || !fast) ? (Dr > 10 ? Dr / 10 : Dr) : kSpmvD;
-        const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
-                                         static_cast<size_t>(Dx + 1) * 4 * 32 * kStencilWarps);
-        if (X == 8) leaves = fused_leaves(v, 32 * kStencilWarps, stage);
-        T* stg = leaves ? stage : nullptr;
-#define ACG_RXM(F, XX, MB)                                                                        \
-    do {                                                                                          \
-        const dim3 g2((v.m + 32 * XX - 1) / (32 * XX),                                            \
-                      (v.m_loc + kStencilWarps / XX - 1) / (kStencilWarps / XX));                 \
-        ensure_smem(k_fused_spmv_ring<T, F, XX, DD, MB>, smem);                                   \
-        k_fused_spmv_ring<T, F, XX, DD, MB><<<g2, block, smem, st>>>(v, u, p, q, z, part, S, stg, leaves); \
-    } while (0)
-#define ACG_RX(F, XX) ACG_RXM(F, XX, 1)
-        if (fast && X == 8 && Dr == 24) {
-            constexpr int DD = 2;
-            ACG_RXM(true, 8, 4);
-        } else if (fast) {
-            constexpr int DD = kSpmvD;
-            if (X == 2) ACG_RX(true, 2); else if (X == 4) ACG_RX(true, 4); else if (X == 8) ACG_RX(true, 8); else ACG_RX(true, 1);
-        } else if (X == 8 && Dr != kSpmvD) {
-            if (Dr == 4) { constexpr int DD = 4; ACG_RX(false, 8); }
-            else if (Dr == 5) { constexpr int DD = 5; ACG_RX(false, 8); }
-            else if (Dr == 2) { constexpr int DD = 2; ACG_RX(false, 8); }
-            else if (Dr == 34) { constexpr int DD = 3; ACG_RXM(false, 8, 4); }
-            else if (Dr == 24) { constexpr int DD = 2; ACG_RXM(false, 8, 4); }
-            else if (Dr == 25) { constexpr int DD = 2; ACG_RXM(false, 8, 5); }
-            else if (Dr == 14) { constexpr int DD = 1; ACG_RXM(false, 8, 4); }
-            else if (Dr == 15) { constexpr int DD = 1; ACG_RXM(false, 8, 5); }
-            else if (Dr == 16) { constexpr int DD = 1; ACG_RXM(false, 8, 6); }
-            else { constexpr int DD = 3; ACG_RX(false, 8); }
-        } else {
-            constexpr int DD = kSpmvD;
-            if (X == 2) ACG_RX(false, 2); else if (X == 4) ACG_RX(false, 4); else if (X == 8) ACG_RX(false, 8); else ACG_RX(false, 1);
-        }
-#undef ACG_RX
-#undef ACG_RXM
     } else {
+        constexpr int D = 5;  // shared z-tile ring depth
+        const dim3 grid((v.m + 31) / 32, (v.m_loc + kStencilWarps - 1) / kStencilWarps);
         const size_t smem = spmv_tile_smem_bytes<T, kStencilWarps>(v.n_z);
-#define ACG_SP(F, DD)                                                                   \
-    do {                                                                                \
-        ensure_smem(k_fused_spmv_tile<T, F, kStencilWarps, DD>, smem);                  \
-        k_fused_spmv_tile<T, F, kStencilWarps, DD><<<grid, block, smem, st>>>(v, u, p, q, z, part, S); \
-    } while (0)
         if (fast) {
-            if (tile_d == 4) ACG_SP(true, 4); else if (tile_d == 6) ACG_SP(true, 6); else ACG_SP(true, 5);
+            ensure_smem(k_fused_spmv_tile<T, true, kStencilWarps, D>, smem);
+            k_fused_spmv_tile<T, true, kStencilWarps, D><<<grid, block, smem, st>>>(v, u, p, q, z,
+                                                                                  part, S);
         } else {
-            if (tile_d == 4) ACG_SP(false, 4); else if (tile_d == 6) ACG_SP(false, 6); else ACG_SP(false, 5);
+            ensure_smem(k_fused_spmv_tile<T, false, kStencilWarps, D>, smem);
+            k_fused_spmv_tile<T, false, kStencilWarps, D><<<grid, block, smem, st>>>(v, u, p, q, z,
+                                                                                   part, S);
         }
-#undef ACG_SP
     }
     post_launch("fused_spmv");
     return leaves;
@@ -1771,15 +1354,9 @@ bool launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
                         cudaStream_t st, const IpcPut<T>* put) {
     IpcPut<T> pp = put ? *put : IpcPut<T>{nullptr, nullptr, 0, 0, 0};
     const int nl = plan.blocks;  // power of two
-    static const bool legacy = [] {
-        const char* e = std::getenv("ACG_TREE2");
-        return e && std::string(e) == "legacy";
-    }();
-    static const bool shfl = [] {
-        const char* e = std::getenv("ACG_TREE2");
-        return e && std::string(e) == "shfl";
-    }();
-    if (!legacy && !shfl && nv <= 2 && nl > 1024 * 8 && nl <= 1024 * 8 * 1024) {
+    // k_tree2_wide (<= 8192 leaves; above, k_tree_mid first) for the sweeps' one or
+    // two values; k_tree2_shfl for three values (<= 16384 leaves); k_tree2 beyond
+    if (nv <= 2 && nl > 1024 * 8 && nl <= 1024 * 8 * 1024) {
         // more leaves than one CTA takes: aligned nodes of 8192 leaves first
         const int nb = nl / 8192;
         T* mid = const_cast<T*>(stage) + static_cast<long long>(nv) * nl;
@@ -1790,7 +1367,7 @@ bool launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
         return launch_tree_stage2<T>(p2, mid, nv, gather, slab, finish, nslabs, exact_tree, S, op,
                                      st, put);
     }
-    if (!legacy && !shfl && nv <= 2 && nl <= 1024 * 8) {
+    if (nv <= 2 && nl <= 1024 * 8) {
         const int c = nl > 1024 ? nl / 1024 : 1;
         const int nt = nl / c;
         const int f = finish ? 1 : 0, ex = exact_tree ? 1 : 0;
@@ -1804,7 +1381,7 @@ bool launch_tree_stage2(const TreePlan& plan, const T* stage, int nv, T* gather,
         return pp.wait != nullptr;
     }
     pp.wait = nullptr;  // the other stage-2 kernels only put; k_finish waits and combines
-    if ((!legacy || pp.n > 0) && nl <= 256 * 64) {
+    if (nl <= 256 * 64) {
         const int c = nl > 256 ? nl / 256 : 1;
         const int nt = nl / c;
         const int f = finish ? 1 : 0, ex = exact_tree ? 1 : 0;

@@ -1031,11 +1031,7 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
         put.n = ip.p;
         put.rank = ip.rank;
         put.seq = seq;
-        static const bool fused_finish = [] {  // ACG_IPC_FINISH=kernel: separate k_finish (A/B)
-            const char* e = std::getenv("ACG_IPC_FINISH");
-            return !(e && std::string(e) == "kernel");
-        }();
-        if (fused_finish && c->slabs.size() == 1) {
+        if (c->slabs.size() == 1) {  // the stage-2 kernel also waits, combines and finishes
             put.wait = ip.flags(ip.rank) + 2;
             put.all = reinterpret_cast<const T*>(ip.gather(ip.rank, par, c->s));
         }
@@ -1867,16 +1863,12 @@ void iterate_interleaved(acg_solver* s) {
             static_cast<T*>(c->slabs[si].part[0]), S[si], static_cast<T*>(c->slabs[si].stage),
             c->stream, f);
     };
-    static const bool overlap_on = [] {
-        const char* e = std::getenv("ACG_HALO_OVERLAP");
-        return !(e && std::string(e) == "0");
-    }();
     const int m_loc0 = c->slabs[0].m_loc;
     if (hl.on) {
         s->ktimer.begin(kFusedSpmv);
         leaves[0] = spmv(0, 0, 0, nullptr);
         s->ktimer.end(kFusedSpmv);
-    } else if (c->halo_stream && overlap_on && m_loc0 >= 3 &&
+    } else if (c->halo_stream && m_loc0 >= 3 &&
         spmv_plane_ranges<T>(view<T>(c, 0), c->fast())) {
         // ranks > 1: the ghost planes travel on the halo stream while the interior
         // planes (which never read a ghost) are swept; the two boundary planes follow

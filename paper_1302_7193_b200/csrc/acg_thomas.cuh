@@ -28,77 +28,6 @@ __device__ __forceinline__ void cpa(T* sdst, const T* gsrc) {
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
-// L2 eviction priorities: data read once (old r, q; the re-read z', r*) is
-// evict-first; the z' / r* the back substitution needs again is evict-last.
-__device__ __forceinline__ unsigned long long policy_evict_first() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_normal() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_last() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-// Cache-policy operands are compiled in only when enabled (scripts/micro/hint_test.cu
-// probes which forms the device accepts).
-#ifndef ACG_L2_HINTS
-#define ACG_L2_HINTS 0
-#endif
-constexpr bool kL2Hints = ACG_L2_HINTS != 0;
-
-template <typename T>
-__device__ __forceinline__ void cpa_hint(T* sdst, const T* gsrc, unsigned long long pol) {
-    if constexpr (!kL2Hints) {
-        cpa(sdst, gsrc);
-        return;
-    }
-    // The policy is created inside the same asm block: ptxas otherwise may place
-    // a long-lived policy in an odd uniform-register pair (scripts/sass_lint.py).
-    (void)pol;
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
-    if constexpr (sizeof(T) == 8)
-        asm volatile(
-            "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-            " cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, pol;\n}\n" ::"r"(sa),
-            "l"(gsrc)
-            : "memory");
-    else
-        asm volatile(
-            "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-            " cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, pol;\n}\n" ::"r"(sa),
-            "l"(gsrc)
-            : "memory");
-}
-__device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
-    if constexpr (!kL2Hints) {
-        *p = v;
-        return;
-    }
-    (void)pol;
-    asm volatile(
-        "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
-        " st.global.L2::cache_hint.f64 [%0], %1, pol;\n}\n" ::"l"(p),
-        "d"(v)
-        : "memory");
-}
-__device__ __forceinline__ void st_hint(float* p, float v, unsigned long long pol) {
-    if constexpr (!kL2Hints) {
-        *p = v;
-        return;
-    }
-    (void)pol;
-    asm volatile(
-        "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
-        " st.global.L2::cache_hint.f32 [%0], %1, pol;\n}\n" ::"l"(p),
-        "f"(v)
-        : "memory");
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -143,14 +72,9 @@ __global__ void __launch_bounds__(C::NT)
     k_thomas(const SlabView<T> v, T* __restrict__ r, const T* __restrict__ in,
              T* __restrict__ out, T* __restrict__ part_r2, T* __restrict__ part_k,
              Scalars<T>* __restrict__ S, const Scalars<T>* __restrict__ gate,
-             T* __restrict__ phi_g, int hints) {
+             T* __restrict__ phi_g) {
     using A = Ar<T, Fast>;
     constexpr int NT = C::NT, NS = C::NS, D = C::D, CP = C::CP;
-    unsigned long long pf = 0, pl = 0;
-    if constexpr (kL2Hints) {
-        pf = hints ? policy_evict_first() : policy_evict_normal();
-        pl = hints ? policy_evict_last() : policy_evict_normal();
-    }
     if (Fused ? S->done != 0 : (gate != nullptr && gate->done != 0)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* prof = reinterpret_cast<T*>(smem_raw);
@@ -191,8 +115,8 @@ __global__ void __launch_bounds__(C::NT)
 #pragma unroll
     for (int t = 0; t < D; ++t) {
         if (t < n_z) {
-            cpa_hint(ring + (2 * t) * NT, ia + t * sm, pf);
-            if (Fused) cpa_hint(ring + (2 * t + 1) * NT, ib + t * sm, pf);
+            cpa(ring + (2 * t) * NT, ia + t * sm);
+            if (Fused) cpa(ring + (2 * t + 1) * NT, ib + t * sm);
         }
         cp_commit();
     }
@@ -209,8 +133,8 @@ __global__ void __launch_bounds__(C::NT)
         const T a0 = ring[0];
         const T a1 = Fused ? ring[NT] : T(0);
         if (D < n_z) {
-            cpa_hint(ring + (2 * D) * NT, ia_n, pf);
-            if (Fused) cpa_hint(ring + (2 * D + 1) * NT, ib_n, pf);
+            cpa(ring + (2 * D) * NT, ia_n);
+            if (Fused) cpa(ring + (2 * D + 1) * NT, ib_n);
         }
         cp_commit();
         ia_n += sm;
@@ -232,8 +156,8 @@ __global__ void __launch_bounds__(C::NT)
             zp = Fused ? A::div(num, A::mul(A::mul(D0, area), dP[0]))
                        : A::div(A::div(num, A::mul(area, dP[0])), D0);
         }
-        if (Fused) st_hint(r_st, rs, pl);
-        st_hint(o_st, zp, pl);
+        if (Fused) *r_st = rs;
+        *o_st = zp;
         r_st += sm;
         o_st += sm;
         if (GPhi) pg[0] = phi; else phs[0] = phi;
@@ -247,8 +171,8 @@ __global__ void __launch_bounds__(C::NT)
             const T a0 = ring[(2 * t) * NT];
             const T a1 = Fused ? ring[(2 * t + 1) * NT] : T(0);
             if (k + D < n_z) {
-                cpa_hint(ring + (2 * ((t + D) % NS)) * NT, ia_n, pf);
-                if (Fused) cpa_hint(ring + (2 * ((t + D) % NS) + 1) * NT, ib_n, pf);
+                cpa(ring + (2 * ((t + D) % NS)) * NT, ia_n);
+                if (Fused) cpa(ring + (2 * ((t + D) % NS) + 1) * NT, ib_n);
             }
             cp_commit();
             ia_n += sm;
@@ -269,8 +193,8 @@ __global__ void __launch_bounds__(C::NT)
                 phi = A::div(bP[k], Dk);
                 zp = A::div(A::sub(A::div(num, A::mul(area, dP[k])), A::mul(cP[k], zp)), Dk);
             }
-            if (Fused) st_hint(r_st, rs, pl);
-            st_hint(o_st, zp, pl);
+            if (Fused) *r_st = rs;
+            *o_st = zp;
             r_st += sm;
             o_st += sm;
             if (t % CP == 0) {
@@ -302,8 +226,8 @@ __global__ void __launch_bounds__(C::NT)
             const int k = top - t;
             if (k >= 0) {
                 const int s = k & (NS - 1);
-                cpa_hint(ring + (2 * s) * NT, oa, pf);
-                if (Fused) cpa_hint(ring + (2 * s + 1) * NT, ra, pf);
+                cpa(ring + (2 * s) * NT, oa);
+                if (Fused) cpa(ring + (2 * s + 1) * NT, ra);
             }
             cp_commit();
             oa -= sm;
@@ -336,8 +260,8 @@ __global__ void __launch_bounds__(C::NT)
             const T rk = Fused ? ring[(2 * t + 1) * NT] : T(0);
             if (k - D >= 0) {
                 const int s = (t + NS - D) % NS;
-                cpa_hint(ring + (2 * s) * NT, oa_n, pf);
-                if (Fused) cpa_hint(ring + (2 * s + 1) * NT, ra_n, pf);
+                cpa(ring + (2 * s) * NT, oa_n);
+                if (Fused) cpa(ring + (2 * s + 1) * NT, ra_n);
             }
             cp_commit();
             oa_n -= sm;

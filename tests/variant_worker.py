@@ -1,10 +1,8 @@
 """Worker for tests/test_variants.py: one process per kernel-variant setting.
 
-The kernel choices (K1 Thomas sweep, K2 stencil sweep, reduction stage 2,
-launch mode) are read once per process from ACG_* environment variables, so
-each variant runs in its own process. It runs the fused sweeps, apply,
-precondition and two full solves (fp64 and fp32, one shape a multiple of the
-CTA widths and one ragged) and compares them bit for bit with the CPU oracle.
+The launch-mode switches (ACG_PDL, ACG_CTA_FINISH) are read once per process,
+so each setting runs in its own process. It runs the fused sweeps, apply,
+precondition and two full solves (fp64 and fp32, over SHAPES) and compares them bit for bit with the CPU oracle.
 Prints VARIANT_OK or the first mismatch.
 """
 import os
@@ -56,8 +54,14 @@ def check(m, n_z, dtype):
     return None
 
 
+# (m, n_z) reaching every shipped kernel: even / ragged widths (pair kernels,
+# TMEM sweeps), odd m (k_fused_spmv_tile; k_thomas_tm for fp32), fp64 columns
+# taller than TMEM holds (k_thomas, z' in global memory), fp32 ones too (n_z 300)
+SHAPES = ((128, 24), (66, 19), (65, 12), (32, 160), (16, 300))
+
+
 def main():
-    for m, n_z in ((128, 24), (66, 19)):
+    for m, n_z in SHAPES:
         for dt in (np.float64, np.float32):
             bad = check(m, n_z, dt)
             if bad:
