@@ -53,9 +53,17 @@ def main():
                     u, r = acg.solve(ctx, f, epsilon=eps, maxiter=40, variant=variant)
                     if math == "exact":
                         uo, ro = o.solve(f, epsilon=eps, maxiter=40, variant=variant)
-                        assert r.iterations == ro.iterations, (m, n_z, dt, variant)
-                        assert np.array_equal(r.residual_history, ro.residual_history)
-                        assert np.array_equal(u, uo)
+                        tag = (m, n_z, np.dtype(dt).name, variant, math, slabs)
+                        if ctx.info["exact_tree"]:  # slabs are reduction-tree nodes: same bits
+                            assert r.iterations == ro.iterations, tag
+                            assert np.array_equal(r.residual_history, ro.residual_history), tag
+                            assert np.array_equal(u, uo), tag
+                        else:  # slab sums combined pairwise: the north-star tolerances
+                            tol = 1e-10 if dt == np.float64 else 1e-4
+                            n = min(len(r.residual_history), len(ro.residual_history))
+                            assert abs(r.iterations - ro.iterations) <= 1, tag
+                            assert (np.abs(r.residual_history[:n] - ro.residual_history[:n]).max()
+                                    <= tol * ro.residual_history[0]), tag
                 if dt == np.float64 and math == "exact":  # the CSR backend (acg_csr.cuh)
                     u, r = acg.solve(ctx, f, epsilon=eps, maxiter=40, variant="standard",
                                      backend="csr")
