@@ -355,12 +355,18 @@ def run_gpu(args, cfg):
     # per-launch K1/K2 events cost ~1% of the step (they sit between the PDL
     # launches), so the headline pass runs without them and a second pass of
     # the same K steps times every K1/K2 launch for the roofline
+    host = {}
+
     def timed_pass():
         solver.time_kernels(args.ktime_inline)
         launches_before = capi.launch_count()
         with ClockSampler(dev) as clk:
             ev0.record(stream)
+            h0 = time.perf_counter()
             solver.iterate(args.steps)
+            # host time to enqueue the K steps: close to the device time means
+            # the host, not the GPU, sets the pace (small grids)
+            host["enqueue_ms"] = (time.perf_counter() - h0) * 1e3
             ev1.record(stream)
             ev1.synchronize()
         barrier()
@@ -529,6 +535,7 @@ def run_gpu(args, cfg):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "sustained": sustained,
             "verified_vs_1gpu": verified,
             "gpu_launches": launches_timed, "clocks": dict(clk.summary(), remeasured=remeasured),
+            "host_enqueue_ms": host.get("enqueue_ms"),
             "exact_tree": bool(info["exact_tree"]),
             "residual_after": float(res["residual_history"][-1]) if res["residual_history"].size else None,
         }

@@ -22,10 +22,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "acg_internal.h"
 
@@ -948,11 +950,34 @@ inline void post_launch(const char* what) {
 
 #include "acg_stencil_tile.cuh"
 
+// Opt a kernel in to more than 48 KB of dynamic shared memory. The attribute is
+// set once per kernel and size (a driver call per launch costs host time the
+// small grids, which are host-paced, cannot afford).
 template <typename KernelT>
 void ensure_smem(KernelT kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(bytes));
+    if (bytes <= 48 * 1024) return;
+    struct Applied {
+        const void* kernel;
+        int device;
+        size_t bytes;
+    };
+    static std::mutex mu;
+    static std::vector<Applied> set;  // attributes are per device context
+    const void* key = reinterpret_cast<const void*>(kernel);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (Applied& e : set)
+        if (e.kernel == key && e.device == dev) {
+            if (e.bytes >= bytes) return;
+            e.bytes = bytes;
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes));
+            return;
+        }
+    set.push_back({key, dev, bytes});
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(bytes));
 }
 
 
@@ -1210,7 +1235,10 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
     }
     if (spmv_pairs(v.m)) {
         constexpr int kCols = 2 * 32 * kStencilWarps;  // columns per CTA (one i-plane)
-        leaves = fused_leaves(v, kCols, stage);
+        // tree node per CTA: kCols columns, or the whole plane of a narrower
+        // power-of-two panel (pair_node_sums)
+        const bool narrow = v.m < kCols && v.m >= 64 && (v.m & (v.m - 1)) == 0;
+        leaves = fused_leaves(v, narrow ? v.m : kCols, stage);
         T* stg = leaves ? stage : nullptr;
         const dim3 g2((v.m + kCols - 1) / kCols, v.plane_count ? v.plane_count : v.m_loc);
         if (sizeof(T) == 4) {

@@ -1622,9 +1622,16 @@ struct acg_solver {
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
     std::vector<int> leaves;  // per slab: tree leaves the last sweep wrote (fused stage 1)
     bool csr = false;         // matrix-explicit backend (standard loop on CSR + tridiagonals)
+    // CUDA graph of kGraphChunk iterations (single-process contexts, small grids):
+    // replayed instead of re-launching the same kernels every iteration
+    cudaGraphExec_t chunk = nullptr;
+    long long chunk_launches = 0;  // kernels per replay (for the launch counter)
+    bool chunk_failed = false;
+    int chunk_kind = -1;           // variant * 2 + csr the graph was captured for
     std::chrono::steady_clock::time_point t0;
     double setup_s = 0.0;
     ~acg_solver() {
+        if (chunk) cudaGraphExecDestroy(chunk);
         for (acg_field* fl : {u, r, z, p, q})
             if (fl) free_field(fl);
         for (void* s : S) cudaFree(s);
@@ -1927,7 +1934,7 @@ void iterate_standard(acg_solver* s) {
 }
 
 template <typename T>
-void solver_iterate(acg_solver* s, int n) {
+void solver_iterate_direct(acg_solver* s, int n) {
     for (int it = 0; it < n; ++it) {
         if (s->cfg.variant == ACG_VARIANT_INTERLEAVED)
             iterate_interleaved<T>(s);
@@ -1935,6 +1942,80 @@ void solver_iterate(acg_solver* s, int n) {
             iterate_standard<T>(s);
     }
     CK(cudaPeekAtLastError());
+}
+
+constexpr int kGraphChunk = 16;
+
+double bytes_per_iteration(const acg_context* c);
+
+// Small grids replay a CUDA graph of kGraphChunk iterations instead of
+// launching 4-5 kernels per iteration from the host: C1 (128^2 x 64) 45.1 ->
+// 41.6 us per iteration; no change at C2/C3 (scripts/gpu_graph_ab.sh), so
+// graphs are used below ~80 us of HBM traffic per iteration. Replay applies
+// where every launch of an iteration is the same from one iteration to the
+// next: one process (the peer-memory and NCCL transports put per-iteration
+// sequence numbers into kernel arguments) and no per-launch event timers.
+bool graph_wanted(const acg_solver* s) {
+    return !s->chunk_failed && s->ctx->comm == nullptr && !s->timer.on && !s->ktimer.on &&
+           bytes_per_iteration(s->ctx) < 0.5e9;
+}
+
+template <typename T>
+bool build_chunk(acg_solver* s) {
+    const acg_context* c = s->ctx;
+    cudaGraph_t g = nullptr;
+    const long long l0 = g_launches.load();
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    bool ok = true;
+    try {
+        solver_iterate_direct<T>(s, kGraphChunk);
+    } catch (const Fail&) {
+        ok = false;
+    }
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (!ok || e != cudaSuccess || !g) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        g_launches -= g_launches.load() - l0;
+        return false;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&s->chunk, g, 0);
+    cudaGraphDestroy(g);
+    s->chunk_launches = g_launches.load() - l0;
+    g_launches -= s->chunk_launches;  // counted per replay instead
+    if (ei != cudaSuccess) {
+        cudaGetLastError();
+        s->chunk = nullptr;
+        return false;
+    }
+    return true;
+}
+
+template <typename T>
+void solver_iterate(acg_solver* s, int n) {
+    if (n >= kGraphChunk && graph_wanted(s)) {
+        const int kind = s->cfg.variant * 2 + (s->csr ? 1 : 0);
+        if (s->chunk && s->chunk_kind != kind) {  // a cached solver reused for another loop
+            cudaGraphExecDestroy(s->chunk);
+            s->chunk = nullptr;
+        }
+        if (!s->chunk) {
+            if (build_chunk<T>(s))
+                s->chunk_kind = kind;
+            else
+                s->chunk_failed = true;
+        }
+        if (s->chunk) {
+            for (; n >= kGraphChunk; n -= kGraphChunk) {
+                CK(cudaGraphLaunch(s->chunk, s->ctx->stream));
+                g_launches += s->chunk_launches;
+            }
+        }
+    }
+    solver_iterate_direct<T>(s, n);
 }
 
 double bytes_per_iteration(const acg_context* c) {

@@ -159,6 +159,25 @@ __device__ __forceinline__ void st_pair_cs(float* a, const Pair<float>& v) {
     __stcs(reinterpret_cast<float2*>(a), make_float2(v.x, v.y));
 }
 
+// Fused reduction stage 1 of the pair sweeps: the CTA's columns [j0, j0 + CW)
+// of plane il (CW = 2 NT = 512) are one node of the pairwise tree; a narrower
+// power-of-two panel (m < CW) makes the plane's m columns the node instead, so
+// small grids keep the fused reduction (no k_tree1 launch). `red` holds the
+// CTA's column partials in column order.
+template <typename T, int CW>
+__device__ __forceinline__ void pair_node_sums(const T* red, T* stage, int nleaves, int il, int m) {
+    if (m >= CW) {
+        cta_subtree_sums<T, CW>(red, 1, stage, nleaves,
+                                (static_cast<long long>(il) * m + blockIdx.x * CW) / CW);
+        return;
+    }
+    switch (m) {  // blockIdx.x == 0: the node is the whole plane
+        case 256: cta_subtree_sums<T, 256>(red, 1, stage, nleaves, il); break;
+        case 128: cta_subtree_sums<T, 128>(red, 1, stage, nleaves, il); break;
+        default: cta_subtree_sums<T, 64>(red, 1, stage, nleaves, il); break;
+    }
+}
+
 // K2 with two adjacent columns per thread (default for fp32): every stream
 // moves the pair as one 8-byte (fp32) / 16-byte (fp64) vector, so the
 // per-thread bookkeeping is paid once per two columns. CTA = one i-plane x
@@ -280,8 +299,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         red[2 * tid + 1] = sigb;
         __syncthreads();
         if (threadIdx.y == 0)
-            cta_subtree_sums<T, 2 * NT>(red, 1, stage, nleaves,
-                                        (static_cast<long long>(il) * m + blockIdx.x * 2 * NT) / (2 * NT));
+            pair_node_sums<T, 2 * NT>(red, stage, nleaves, il, m);
         return;
     }
     *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};
@@ -400,8 +418,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         red[2 * tid + 1] = sigb;
         __syncthreads();
         if (threadIdx.y == 0)
-            cta_subtree_sums<T, 2 * NT>(red, 1, stage, nleaves,
-                                        (static_cast<long long>(il) * m + blockIdx.x * 2 * NT) / (2 * NT));
+            pair_node_sums<T, 2 * NT>(red, stage, nleaves, il, m);
         if (fin.op >= 0) cta_finish(fin, stage, nleaves, 1, red, tid, NT);
         return;
     }

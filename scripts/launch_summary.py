@@ -14,9 +14,10 @@ for lid, m in per.items():
     t, u = m["gpu__time_duration.sum"]
     t = t / 1e3 if u == "nsecond" else (t * 1e3 if u == "msecond" else t)  # -> usecond
     a = agg[name]
-    a[0] += 1; a[1] += t; a[2] += m["dram__bytes_read.sum"][0]; a[3] += m["dram__bytes_write.sum"][0]
+    a[0] += 1; a[1] += t
+    a[2] += m.get("dram__bytes_read.sum", (0.0, ""))[0]; a[3] += m.get("dram__bytes_write.sum", (0.0, ""))[0]
 tot = sum(a[1] for a in agg.values())
-print(f"{'kernel':60s} {'launches':>8s} {'mean_ns':>10s} {'share':>7s} {'rd/launch':>10s} {'wr/launch':>10s}")
+print(f"{'kernel':60s} {'launches':>8s} {'mean_us':>10s} {'share':>7s} {'rd/launch':>10s} {'wr/launch':>10s}")
 for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     unit = 1.0
     print(f"{name[:60]:60s} {a[0]:8d} {a[1]/a[0]:10.1f} {a[1]/tot*100:6.1f}% {a[2]/a[0]:10.3g} {a[3]/a[0]:10.3g}")
