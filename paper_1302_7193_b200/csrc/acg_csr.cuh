@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256)
         const long long e0 = row_ptr[r], e1 = row_ptr[r + 1];
         T sum = T(0);
         for (long long e = e0; e < e1; ++e)
-            sum = A::add(sum, A::mul(__ldcs(vals + e), x[__ldcs(col_idx + e)]));
+            sum = A::add(sum, A::mul(vals[e], x[col_idx[e]]));
         y[r] = sum;
     }
 }

@@ -223,75 +223,77 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     T* pc = p + base;
     T* qc = q + base;
     const long long sm = m;
-    auto issue = [&](int k, int s) {
-        const long long l = static_cast<long long>(k) * sm;
-        P* r0 = ring + s * 4 * NT;
-        cpa_pair<T>(r0, pc + l);
-        cpa_pair<T>(r0 + NT, qc + l);
-        cpa_pair<T>(r0 + 2 * NT, uc + l);
-        if (k + 1 < n_z) cpa_pair<T>(r0 + 3 * NT, zc + l + sm);
-    };
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        if (t < n_z) issue(t, t);
-        cp_commit();
-    }
-    P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
     T siga = T(0), sigb = T(0);
-    // outside neighbours one level ahead: i+-1 rows as pairs, z(j-1), z(j+2)
-    long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
-    if (v.halo.on) {  // ghost rows straight from this rank's mailbox
-        if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
-        if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
-    }
-    // i+-1 rows through L2 (coherent: the ghost rows may be a peer's fresh stores)
-    P ze = ldcg_pair<T>(zc + oe), zw = ldcg_pair<T>(zc + ow);
-    T zs = zc[ca.os], zn = zc[1 + cb.on];
-    int cs = 0, ps_ = D;
-    for (int k = 0; k < n_z; ++k) {
-        const long long l = static_cast<long long>(k) * sm;
-        const P ce = ze, cw = zw;
-        const T cs0 = zs, cn1 = zn;
-        if (k + 1 < n_z) {
-            const long long l1 = l + sm;
-            ze = ldcg_pair<T>(zc + l1 + oe);
-            zw = ldcg_pair<T>(zc + l1 + ow);
-            zs = zc[l1 + ca.os];
-            zn = zc[l1 + 1 + cb.on];
+    if (valid) {  // the idle warps of a narrow panel's CTA (fused reduction) skip the sweep
+        auto issue = [&](int k, int s) {
+            const long long l = static_cast<long long>(k) * sm;
+            P* r0 = ring + s * 4 * NT;
+            cpa_pair<T>(r0, pc + l);
+            cpa_pair<T>(r0 + NT, qc + l);
+            cpa_pair<T>(r0 + 2 * NT, uc + l);
+            if (k + 1 < n_z) cpa_pair<T>(r0 + 3 * NT, zc + l + sm);
+        };
+    #pragma unroll
+        for (int t = 0; t < D; ++t) {
+            if (t < n_z) issue(t, t);
+            cp_commit();
         }
-        cp_wait<D - 1>();
-        const P* r0 = ring + cs * 4 * NT;
-        P pv = r0[0], qv = r0[NT];
-        const P uv = r0[2 * NT];
-        const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
-        if (k + D < n_z) issue(k + D, ps_);
-        cp_commit();
-        cs = cs + 1 == NS ? 0 : cs + 1;
-        ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
-        const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
-        pv.x = A::add(A::mul(beta, pv.x), z0.x);
-        pv.y = A::add(A::mul(beta, pv.y), z0.y);
-        qv.x = A::mul(beta, qv.x);
-        qv.y = A::mul(beta, qv.y);
-        // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
-        const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
-                                       ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
-        // column j+1: south = own .x, north = z(j+2) (own value on the edge)
-        const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
-                                       cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
-        qv.x = A::add(qv.x, A::mul(dP[k], dqa));
-        qv.y = A::add(qv.y, A::mul(dP[k], dqb));
-        siga = A::add(siga, A::mul(pv.x, qv.x));
-        sigb = A::add(sigb, A::mul(pv.y, qv.y));
-        if (valid) {
-            st_pair_cs(uc + l, un);
-            st_pair_cs(pc + l, pv);
-            st_pair_cs(qc + l, qv);
+        P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
+        // outside neighbours one level ahead: i+-1 rows as pairs, z(j-1), z(j+2)
+        long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+        if (v.halo.on) {  // ghost rows straight from this rank's mailbox
+            if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
+            if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
         }
-        zd = z0;
-        z0 = zu;
+        // i+-1 rows through L2 (coherent: the ghost rows may be a peer's fresh stores)
+        P ze = ldcg_pair<T>(zc + oe), zw = ldcg_pair<T>(zc + ow);
+        T zs = zc[ca.os], zn = zc[1 + cb.on];
+        int cs = 0, ps_ = D;
+        for (int k = 0; k < n_z; ++k) {
+            const long long l = static_cast<long long>(k) * sm;
+            const P ce = ze, cw = zw;
+            const T cs0 = zs, cn1 = zn;
+            if (k + 1 < n_z) {
+                const long long l1 = l + sm;
+                ze = ldcg_pair<T>(zc + l1 + oe);
+                zw = ldcg_pair<T>(zc + l1 + ow);
+                zs = zc[l1 + ca.os];
+                zn = zc[l1 + 1 + cb.on];
+            }
+            cp_wait<D - 1>();
+            const P* r0 = ring + cs * 4 * NT;
+            P pv = r0[0], qv = r0[NT];
+            const P uv = r0[2 * NT];
+            const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
+            if (k + D < n_z) issue(k + D, ps_);
+            cp_commit();
+            cs = cs + 1 == NS ? 0 : cs + 1;
+            ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
+            const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
+            pv.x = A::add(A::mul(beta, pv.x), z0.x);
+            pv.y = A::add(A::mul(beta, pv.y), z0.y);
+            qv.x = A::mul(beta, qv.x);
+            qv.y = A::mul(beta, qv.y);
+            // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
+            const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
+                                           ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
+            // column j+1: south = own .x, north = z(j+2) (own value on the edge)
+            const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
+                                           cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
+            qv.x = A::add(qv.x, A::mul(dP[k], dqa));
+            qv.y = A::add(qv.y, A::mul(dP[k], dqb));
+            siga = A::add(siga, A::mul(pv.x, qv.x));
+            sigb = A::add(sigb, A::mul(pv.y, qv.y));
+            if (valid) {
+                st_pair_cs(uc + l, un);
+                st_pair_cs(pc + l, pv);
+                st_pair_cs(qc + l, qv);
+            }
+            zd = z0;
+            z0 = zu;
+        }
+        cp_wait<0>();
     }
-    cp_wait<0>();
     if (stage != nullptr) {  // fused reduction stage 1: the CTA's 512 columns are a tree node
         __syncthreads();
         T* red = prof + 4 * n_z;
@@ -347,70 +349,72 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     T* pc = p + base;
     T* qc = q + base;
     const long long sm = m;
-    long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
-    if (v.halo.on) {  // ghost rows straight from this rank's mailbox
-        if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
-        if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
-    }
-    auto issue = [&](int k, int s) {
-        const long long l = static_cast<long long>(k) * sm;
-        P* r0 = ring + s * 7 * NT;
-        cpa_pair<T>(r0, pc + l);
-        cpa_pair<T>(r0 + NT, qc + l);
-        cpa_pair<T>(r0 + 2 * NT, uc + l);
-        if (k + 1 < n_z) cpa_pair<T>(r0 + 3 * NT, zc + l + sm);
-        cpa_pair<T>(r0 + 4 * NT, zc + l + oe);
-        cpa_pair<T>(r0 + 5 * NT, zc + l + ow);
-        T* e = reinterpret_cast<T*>(r0 + 6 * NT);  // z(j-1), z(j+2) (own values on the edges)
-        cpa(e, zc + l + ca.os);
-        cpa(e + 1, zc + l + 1 + cb.on);
-    };
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        if (t < n_z) issue(t, t);
-        cp_commit();
-    }
-    P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
     T siga = T(0), sigb = T(0);
-    int cs = 0, ps_ = D;
-    for (int k = 0; k < n_z; ++k) {
-        const long long l = static_cast<long long>(k) * sm;
-        cp_wait<D - 1>();
-        const P* r0 = ring + cs * 7 * NT;
-        P pv = r0[0], qv = r0[NT];
-        const P uv = r0[2 * NT];
-        const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
-        const P ce = r0[4 * NT], cw = r0[5 * NT];
-        const P ex = r0[6 * NT];
-        const T cs0 = ex.x, cn1 = ex.y;
-        if (k + D < n_z) issue(k + D, ps_);
-        cp_commit();
-        cs = cs + 1 == NS ? 0 : cs + 1;
-        ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
-        const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
-        pv.x = A::add(A::mul(beta, pv.x), z0.x);
-        pv.y = A::add(A::mul(beta, pv.y), z0.y);
-        qv.x = A::mul(beta, qv.x);
-        qv.y = A::mul(beta, qv.y);
-        // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
-        const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
-                                       ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
-        // column j+1: south = own .x, north = z(j+2) (own value on the edge)
-        const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
-                                       cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
-        qv.x = A::add(qv.x, A::mul(dP[k], dqa));
-        qv.y = A::add(qv.y, A::mul(dP[k], dqb));
-        siga = A::add(siga, A::mul(pv.x, qv.x));
-        sigb = A::add(sigb, A::mul(pv.y, qv.y));
-        if (valid) {
-            st_pair_cs(uc + l, un);
-            st_pair_cs(pc + l, pv);
-            st_pair_cs(qc + l, qv);
+    if (valid) {  // the idle warps of a narrow panel's CTA (fused reduction) skip the sweep
+        long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+        if (v.halo.on) {  // ghost rows straight from this rank's mailbox
+            if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
+            if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
         }
-        zd = z0;
-        z0 = zu;
+        auto issue = [&](int k, int s) {
+            const long long l = static_cast<long long>(k) * sm;
+            P* r0 = ring + s * 7 * NT;
+            cpa_pair<T>(r0, pc + l);
+            cpa_pair<T>(r0 + NT, qc + l);
+            cpa_pair<T>(r0 + 2 * NT, uc + l);
+            if (k + 1 < n_z) cpa_pair<T>(r0 + 3 * NT, zc + l + sm);
+            cpa_pair<T>(r0 + 4 * NT, zc + l + oe);
+            cpa_pair<T>(r0 + 5 * NT, zc + l + ow);
+            T* e = reinterpret_cast<T*>(r0 + 6 * NT);  // z(j-1), z(j+2) (own values on the edges)
+            cpa(e, zc + l + ca.os);
+            cpa(e + 1, zc + l + 1 + cb.on);
+        };
+    #pragma unroll
+        for (int t = 0; t < D; ++t) {
+            if (t < n_z) issue(t, t);
+            cp_commit();
+        }
+        P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
+        int cs = 0, ps_ = D;
+        for (int k = 0; k < n_z; ++k) {
+            const long long l = static_cast<long long>(k) * sm;
+            cp_wait<D - 1>();
+            const P* r0 = ring + cs * 7 * NT;
+            P pv = r0[0], qv = r0[NT];
+            const P uv = r0[2 * NT];
+            const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
+            const P ce = r0[4 * NT], cw = r0[5 * NT];
+            const P ex = r0[6 * NT];
+            const T cs0 = ex.x, cn1 = ex.y;
+            if (k + D < n_z) issue(k + D, ps_);
+            cp_commit();
+            cs = cs + 1 == NS ? 0 : cs + 1;
+            ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
+            const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
+            pv.x = A::add(A::mul(beta, pv.x), z0.x);
+            pv.y = A::add(A::mul(beta, pv.y), z0.y);
+            qv.x = A::mul(beta, qv.x);
+            qv.y = A::mul(beta, qv.y);
+            // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
+            const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
+                                           ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
+            // column j+1: south = own .x, north = z(j+2) (own value on the edge)
+            const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
+                                           cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
+            qv.x = A::add(qv.x, A::mul(dP[k], dqa));
+            qv.y = A::add(qv.y, A::mul(dP[k], dqb));
+            siga = A::add(siga, A::mul(pv.x, qv.x));
+            sigb = A::add(sigb, A::mul(pv.y, qv.y));
+            if (valid) {
+                st_pair_cs(uc + l, un);
+                st_pair_cs(pc + l, pv);
+                st_pair_cs(qc + l, qv);
+            }
+            zd = z0;
+            z0 = zu;
+        }
+        cp_wait<0>();
     }
-    cp_wait<0>();
     if (stage != nullptr) {  // fused reduction stage 1: the CTA's 512 columns are a tree node
         __syncthreads();
         T* red = prof + 4 * n_z;

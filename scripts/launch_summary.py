@@ -12,7 +12,7 @@ agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0])
 for lid, m in per.items():
     name = m["name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "").replace("acg::", "")
     t, u = m["gpu__time_duration.sum"]
-    t = t / 1e3 if u == "nsecond" else (t * 1e3 if u == "msecond" else t)  # -> usecond
+    t = t / 1e3 if u in ("ns", "nsecond") else (t * 1e3 if u in ("ms", "msecond") else t)  # -> usecond
     a = agg[name]
     a[0] += 1; a[1] += t
     a[2] += m.get("dram__bytes_read.sum", (0.0, ""))[0]; a[3] += m.get("dram__bytes_write.sum", (0.0, ""))[0]
