@@ -120,7 +120,7 @@ void nccl_check(ncclResult_t r, const char* what) {
 }  // namespace
 
 struct acg_comm {
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;  // NULL after a failed call aborted it (ncclCommAbort)
     int rank = 0, nranks = 1, device = 0;
     int kind = 0;           // 0: NCCL, 1: peer memory (CUDA IPC, one node)
     unsigned char uid[16];  // IPC: rendezvous namespace
@@ -128,6 +128,24 @@ struct acg_comm {
 };
 
 namespace {
+
+// A failed NCCL call on a communicator aborts it (ncclCommAbort releases the
+// other ranks' pending operations instead of leaving them to hang) before the
+// error is reported; later calls on the aborted communicator fail immediately.
+void nccl_comm_check(acg_comm* c, ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return;
+    NcclApi& api = nccl();
+    if (c && c->comm && api.commAbort) {
+        api.commAbort(c->comm);
+        c->comm = nullptr;
+    }
+    fail(ACG_ERR_NCCL, "%s: %s (communicator aborted)", what,
+         api.errorString ? api.errorString(r) : "error");
+}
+
+void nccl_comm_alive(const acg_comm* c) {
+    if (!c->comm) fail(ACG_ERR_NCCL, "NCCL communicator was aborted after an earlier failure");
+}
 
 // Peer-memory transport state of one context (acg_comm_create_ipc). Every rank
 // owns a mailbox: flags (halo from below / above, one reduction flag per rank),
@@ -993,18 +1011,20 @@ void halo(const acg_context* c, const acg_field* f, cudaStream_t hs = nullptr) {
     const Slab& s = c->slabs[0];
     const ncclDataType_t dt = c->dtype == ACG_F32 ? ncclFloat32 : ncclFloat64;
     const size_t cnt = static_cast<size_t>(s.plane);
-    nccl_check(api.groupStart(), "ncclGroupStart");
+    acg_comm* cm = c->comm;
+    nccl_comm_alive(cm);
+    nccl_comm_check(cm, api.groupStart(), "ncclGroupStart");
     if (r > 0) {
-        nccl_check(api.send(plane_ptr(0, 0), cnt, dt, r - 1, c->comm->comm, hs), "ncclSend");
-        nccl_check(api.recv(plane_ptr(0, -1), cnt, dt, r - 1, c->comm->comm, hs), "ncclRecv");
+        nccl_comm_check(cm, api.send(plane_ptr(0, 0), cnt, dt, r - 1, cm->comm, hs), "ncclSend");
+        nccl_comm_check(cm, api.recv(plane_ptr(0, -1), cnt, dt, r - 1, cm->comm, hs), "ncclRecv");
     }
     if (r + 1 < p) {
-        nccl_check(api.send(plane_ptr(0, s.m_loc - 1), cnt, dt, r + 1, c->comm->comm, hs),
-                   "ncclSend");
-        nccl_check(api.recv(plane_ptr(0, s.m_loc), cnt, dt, r + 1, c->comm->comm, hs),
-                   "ncclRecv");
+        nccl_comm_check(cm, api.send(plane_ptr(0, s.m_loc - 1), cnt, dt, r + 1, cm->comm, hs),
+                        "ncclSend");
+        nccl_comm_check(cm, api.recv(plane_ptr(0, s.m_loc), cnt, dt, r + 1, cm->comm, hs),
+                        "ncclRecv");
     }
-    nccl_check(api.groupEnd(), "ncclGroupEnd");
+    nccl_comm_check(cm, api.groupEnd(), "ncclGroupEnd");
 }
 
 // -------------------------------------------------------------- reductions
@@ -1063,8 +1083,10 @@ void reduce(const acg_context* c, int nv, int op, const std::vector<Scalars<T>*>
         gather = reinterpret_cast<T*>(ip.gather(ip.rank, par, c->s));
     } else if (c->comm) {
         const ncclDataType_t dt = c->dtype == ACG_F32 ? ncclFloat32 : ncclFloat64;
-        nccl_check(nccl().allGather(c->gather_send, c->gather, 4, dt, c->comm->comm, c->stream),
-                   "ncclAllGather");
+        nccl_comm_alive(c->comm);
+        nccl_comm_check(c->comm,
+                        nccl().allGather(c->gather_send, c->gather, 4, dt, c->comm->comm, c->stream),
+                        "ncclAllGather");
     }
     for (size_t si = 0; si < c->slabs.size(); ++si)
         launch_finish<T>(gather, nv, c->nslabs_total, c->exact_tree, S[si], op, c->stream,

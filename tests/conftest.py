@@ -12,6 +12,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running parity case")
+    config.addinivalue_line("markers", "multigpu: needs N > 1 GPUs in one node (skips otherwise)")
 
 
 def gpu_available():

@@ -30,9 +30,14 @@ def main():
     dev = 0 if os.environ.get("ACG_SAME_GPU", "1") == "1" else int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
-    uid = [os.urandom(16) if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    comm = capi.Comm.ipc(rank, world, uid[0], dev)
+    if os.environ.get("ACG_TEST_TRANSPORT") == "nccl":  # one GPU per rank (NCCL refuses shared GPUs)
+        uid = [capi.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = capi.Comm(rank, world, uid[0], dev)
+    else:
+        uid = [os.urandom(16) if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = capi.Comm.ipc(rank, world, uid[0], dev)
     o = Oracle(Problem(m, n_z))
     ctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag, device=dev,
                        comm=comm, dtype=capi.F32 if f32 else capi.F64)
