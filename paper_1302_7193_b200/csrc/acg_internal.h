@@ -125,17 +125,6 @@ TreePlan make_tree_plan(long long n);
 // Dynamic shared memory of one Thomas block (K1/K4) for a column height.
 size_t thomas_smem_per_block(int dsize, int n_z, bool global_phi);
 
-// In-kernel finish of a reduction (single-slab contexts): the sweep's last CTA
-// reduces the tree-node sums it and the other CTAs wrote to `stage` and runs
-// scalar program `op` (the work k_tree2 + run_op would do in a separate launch).
-template <typename T>
-struct Finish {
-    Scalars<T>* S = nullptr;
-    int* counter = nullptr;  // zero between uses; the last CTA resets it
-    int op = -1;
-    bool used = false;       // set by the launcher when the kernel took it over
-};
-
 // ----------------------------------------------------------------- launchers
 extern std::atomic<long long> g_launches;  // kernel launches issued (all entry points)
 
@@ -144,8 +133,7 @@ extern std::atomic<long long> g_launches;  // kernel launches issued (all entry 
 // written to part_* and the reduction runs k_tree1).
 template <typename T>
 int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st,
-                      Finish<T>* fin = nullptr);
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st);
 // Once per slab: may the sweeps use the TMEM kernel with common-path
 // divisions (k_validate_tm)? Synchronous.
 template <typename T>
@@ -171,7 +159,7 @@ template <typename T>
 bool spmv_plane_ranges(const SlabView<T>& v, bool fast);
 template <typename T>
 int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                      const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin = nullptr);
+                      const Scalars<T>* S, T* stage, cudaStream_t st);
 template <typename T>
 void launch_apply(const SlabView<T>& v, bool fast, const T* x, T* y, const Scalars<T>* gate,
                   cudaStream_t st);

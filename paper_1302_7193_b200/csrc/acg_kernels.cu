@@ -227,47 +227,6 @@ __device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __res
 template <typename T>
 __device__ void run_op(Scalars<T>* S, int op, const T* sums);
 
-// Device view of Finish<T> passed to the sweeps (op < 0: off).
-template <typename T>
-struct FinishDev {
-    Scalars<T>* S;
-    int* counter;
-    int op;
-};
-
-// Last-CTA finish (single slab): after every CTA has written its node sums to
-// stage[a * nleaves + leaf], the CTA that arrives last reduces the nleaves
-// (a power of two) of each array with the perfect tree (k_tree2's order) in
-// shared memory `buf` (>= nleaves values) and runs the scalar program.
-template <typename T>
-__device__ void cta_finish(const FinishDev<T>& fin, const T* stage, int nleaves, int nv, T* buf,
-                           int tid, int nthreads) {
-    __shared__ int last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last = atomicAdd(fin.counter, 1) == static_cast<int>(gridDim.x * gridDim.y) - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    T sums[4] = {T(0), T(0), T(0), T(0)};
-    for (int a = 0; a < nv; ++a) {
-        for (int l = tid; l < nleaves; l += nthreads)
-            buf[l] = __ldcg(stage + static_cast<long long>(a) * nleaves + l);
-        __syncthreads();
-        for (int st = 1; st < nleaves; st <<= 1) {
-            for (int i = tid * 2 * st; i < nleaves; i += nthreads * 2 * st)
-                buf[i] = add_rn(buf[i], buf[i + st]);
-            __syncthreads();
-        }
-        sums[a] = buf[0];
-        __syncthreads();
-    }
-    if (tid == 0) {
-        run_op(fin.S, fin.op, sums);
-        *fin.counter = 0;
-    }
-}
-
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
 #include "acg_thomas_tm.cuh"
@@ -1037,8 +996,7 @@ int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
 // beyond that would only wait inside tcgen05.alloc).
 template <typename T, bool Fast, bool Fused, class C>
 int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
-                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st,
-                         Finish<T>* fin = nullptr) {
+                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
     const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
     const dim3 block(32, C::W);
     constexpr int PW = C::W / C::X;  // i-planes per CTA
@@ -1047,7 +1005,7 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     // resident CTAs per SM with a last wave >= 97% full (C3: 4, K1 0.789 ->
     // 0.777 ms; tpc 3, 5, 6 leave a 24-62% last wave: 0.80-0.81 ms; 8: 0.855 ms).
     int tpc = 1;
-    if (C::X == 4 && !v.halo.on && fin == nullptr) {
+    if (C::X == 4 && !v.halo.on) {
         const double slots = 2.0 * num_sms();
         const long long rows = (v.m + 127) / 128;
         for (int t = 4; t > 1; --t) {
@@ -1066,17 +1024,9 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     if (smem < floor_bytes) smem = floor_bytes;
     // fused stage 1: CTA = one aligned node (128 consecutive columns) of the tree
     const int leaves = fused_leaves(v, C::X == 4 ? C::NT : 0, Fused ? stage : nullptr);
-    FinishDev<T> fd{nullptr, nullptr, -1};
-    // the finish tree needs `leaves` values of the (then free) shared memory after the profile
-    if (fin && leaves > 0 &&
-        static_cast<size_t>(leaves) + kTmProf * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
-        fd = {fin->S, fin->counter, fin->op};
-        fin->used = true;
-    }
     ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
     launch_pdl(k_thomas_tm<T, Fast, Fused, C>, grid, block, smem, st, v, r, in, out, p2, pk,
-               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, fd,
-               tpc);
+               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, tpc);
     return leaves;
 }
 
@@ -1115,8 +1065,7 @@ using ThomasTm2Default = ThomasTm2Cfg<4, 15, 15>;
 
 template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
-                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st,
-                  Finish<T>* fin = nullptr) {
+                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
     const bool tmem = v.tm_ok && phi_scratch == nullptr;
     if (tmem && sizeof(T) == 4) {
         const int l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Default>(v, r, in, out, p2, pk,
@@ -1125,7 +1074,7 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
     }
     if (tmem && thomas_tm_cols(v.n_z, sizeof(T)) <= 256)
         return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmDefault>(v, r, in, out, p2, pk, S, gate,
-                                                                    stage, st, fin);
+                                                                    stage, st);
     if (v.halo.on) {  // fused_halo_ok admits only the TMEM sweeps
         std::fprintf(stderr, "acg: fused halo requested for a sweep that cannot carry it\n");
         std::abort();
@@ -1173,13 +1122,12 @@ bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st) {
 
 template <typename T>
 int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st,
-                      Finish<T>* fin) {
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st) {
     const int leaves =
         fast ? launch_thomas<T, true, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
-                                            stage, st, fin)
+                                            stage, st)
              : launch_thomas<T, false, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
-                                             stage, st, fin);
+                                             stage, st);
     post_launch("fused_prec");
     return leaves;
 }
@@ -1226,7 +1174,7 @@ bool spmv_plane_ranges(const SlabView<T>& v, bool fast) {
 
 template <typename T>
 int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                      const Scalars<T>* S, T* stage, cudaStream_t st, Finish<T>* fin) {
+                      const Scalars<T>* S, T* stage, cudaStream_t st) {
     int leaves = 0;
     const dim3 block(32, kStencilWarps);
     if (v.halo.on && !(spmv_pairs(v.m) && v.plane_count == 0)) {
@@ -1260,20 +1208,14 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             constexpr int D = 3;
             const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                              static_cast<size_t>(D + 1) * 7 * kCols);
-            FinishDev<T> fd{nullptr, nullptr, -1};
-            if (fin && leaves > 0 &&
-                static_cast<size_t>(leaves) + 4 * static_cast<size_t>(v.n_z) <= smem / sizeof(T)) {
-                fd = {fin->S, fin->counter, fin->op};
-                fin->used = true;
-            }
             if (fast) {
                 ensure_smem(k_fused_spmv_pair2<T, true, D, 2>, smem);
                 launch_pdl(k_fused_spmv_pair2<T, true, D, 2>, g2, block, smem, st, v, u, p, q, z,
-                           part, S, stg, leaves, fd);
+                           part, S, stg, leaves);
             } else {
                 ensure_smem(k_fused_spmv_pair2<T, false, D, 2>, smem);
                 launch_pdl(k_fused_spmv_pair2<T, false, D, 2>, g2, block, smem, st, v, u, p, q, z,
-                           part, S, stg, leaves, fd);
+                           part, S, stg, leaves);
             }
         }
     } else {
@@ -1467,13 +1409,13 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
 #define ACG_INSTANTIATE(T)                                                                      \
     template bool validate_thomas_tm<T>(const SlabView<T>&, cudaStream_t);                      \
     template int launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,       \
-                                      Scalars<T>*, T*, T*, cudaStream_t, Finish<T>*);           \
+                                      Scalars<T>*, T*, T*, cudaStream_t);                       \
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
                                          const Scalars<T>*, T*, cudaStream_t);                  \
     template bool spmv_plane_ranges<T>(const SlabView<T>&, bool);                               \
     template bool fused_halo_ok<T>(const SlabView<T>&, bool, bool);                              \
     template int launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,       \
-                                      const Scalars<T>*, T*, cudaStream_t, Finish<T>*);         \
+                                      const Scalars<T>*, T*, cudaStream_t);                   \
     template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \
                                   cudaStream_t);                                                \
     template void launch_residual_partials<T>(const SlabView<T>&, bool, const T*, const T*, T*, \

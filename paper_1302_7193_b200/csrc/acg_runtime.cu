@@ -279,7 +279,6 @@ struct Slab {
     void* tmp = nullptr;  // Scalars<T> for API calls
     TreePlan plan{};
     bool tm_ok = false;   // TMEM Thomas sweep usable (validate_thomas_tm)
-    int* fin_counter = nullptr;  // last-CTA finish counter of the fused sweeps (zero at rest)
     // matrix-explicit backend (acg_csr.cuh), assembled on first use per layout
     int csr_layout = -1;
     long long* csr_rp = nullptr;
@@ -450,8 +449,7 @@ void build_slab_tables(const acg_context* c, Slab& s, const acg_operator_desc* d
 
 void free_slab(Slab& s) {
     free_csr(s);
-    void* ps[] = {s.prof, s.col, s.part[0], s.part[1], s.part[2], s.stage, s.phi, s.staging, s.tmp,
-                  s.fin_counter};
+    void* ps[] = {s.prof, s.col, s.part[0], s.part[1], s.part[2], s.stage, s.phi, s.staging, s.tmp};
     for (void* p : ps)
         if (p) cudaFree(p);
     s = Slab{};
@@ -644,8 +642,6 @@ acg_status acg_context_create(acg_context** out, acg_dtype dtype, const acg_oper
             if (s.plan.blocks > 16384)
                 fail(ACG_ERR_INVALID_ARGUMENT, "slab of %lld columns exceeds the reduction plan",
                      ncol);
-            CK(cudaMalloc(&s.fin_counter, sizeof(int)));
-            CK(cudaMemset(s.fin_counter, 0, sizeof(int)));
             // stage: k_tree1 block sums, or up to kMaxFusedLeaves node sums written by a
             // sweep followed by the stage-1.5 nodes
             CK(cudaMalloc(&s.stage,
@@ -1826,15 +1822,6 @@ void iterate_interleaved(acg_solver* s) {
     auto S = sv<T>(s);
     std::vector<int>& leaves = s->leaves;
     leaves.resize(c->slabs.size());
-    // Single slab, opt-in (ACG_CTA_FINISH=1): the sweep's last CTA finishes the
-    // reduction instead of a k_tree2 launch. Measured slower at C3 (2.027 vs
-    // 2.004 ms/iter): the one-CTA tail tree over 8192 leaves costs more than
-    // the launch it saves.
-    static const bool cta_finish = [] {
-        const char* e = std::getenv("ACG_CTA_FINISH");
-        return e && std::string(e) == "1";
-    }();
-    const bool single = c->nslabs_total == 1 && cta_finish;
     // Peer-memory halo fused into the sweeps: K1 stores its boundary
     // planes into the neighbours' mailboxes and releases their flags; K2's boundary
     // CTAs acquire them and read the ghost rows from the local mailbox. No copy or
@@ -1862,7 +1849,6 @@ void iterate_interleaved(acg_solver* s) {
             hl.wait_flag[1] = ip.flags(r) + 1;
         }
     }
-    Finish<T> fin1{S[0], c->slabs[0].fin_counter, kOpIlPrec, false};
     s->timer.begin(kFusedPrec);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& sl = c->slabs[si];
@@ -1873,15 +1859,13 @@ void iterate_interleaved(acg_solver* s) {
             v1, c->fast(), static_cast<T*>(s->r->data(si)),
             static_cast<T*>(s->z->data(si)), static_cast<const T*>(s->q->data(si)),
             static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), S[si],
-            static_cast<T*>(sl.phi), static_cast<T*>(sl.stage), c->stream,
-            single ? &fin1 : nullptr);
+            static_cast<T*>(sl.phi), static_cast<T*>(sl.stage), c->stream);
         s->ktimer.end(kFusedPrec);
     }
-    if (!fin1.used) reduce<T>(c, 2, kOpIlPrec, S, nullptr, true, &leaves);
+    reduce<T>(c, 2, kOpIlPrec, S, nullptr, true, &leaves);
     s->timer.end(kFusedPrec);
     s->timer.begin(kFusedSpmv);
-    Finish<T> fin2{S[0], c->slabs[0].fin_counter, kOpIlSpmv, false};
-    auto spmv = [&](size_t si, int pb, int pc, Finish<T>* f) {
+    auto spmv = [&](size_t si, int pb, int pc) {
         SlabView<T> v = view<T>(c, si);
         v.plane_begin = pb;
         v.plane_count = pc;
@@ -1890,12 +1874,12 @@ void iterate_interleaved(acg_solver* s) {
             v, c->fast(), static_cast<T*>(s->u->data(si)), static_cast<T*>(s->p->data(si)),
             static_cast<T*>(s->q->data(si)), static_cast<const T*>(s->z->data(si)),
             static_cast<T*>(c->slabs[si].part[0]), S[si], static_cast<T*>(c->slabs[si].stage),
-            c->stream, f);
+            c->stream);
     };
     const int m_loc0 = c->slabs[0].m_loc;
     if (hl.on) {
         s->ktimer.begin(kFusedSpmv);
-        leaves[0] = spmv(0, 0, 0, nullptr);
+        leaves[0] = spmv(0, 0, 0);
         s->ktimer.end(kFusedSpmv);
     } else if (c->halo_stream && m_loc0 >= 3 &&
         spmv_plane_ranges<T>(view<T>(c, 0), c->fast())) {
@@ -1906,20 +1890,20 @@ void iterate_interleaved(acg_solver* s) {
         halo(c, s->z, c->halo_stream);
         CK(cudaEventRecord(c->ev_halo, c->halo_stream));
         s->ktimer.begin(kFusedSpmv);
-        leaves[0] = spmv(0, 1, m_loc0 - 2, nullptr);
+        leaves[0] = spmv(0, 1, m_loc0 - 2);
         CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
-        spmv(0, 0, 1, nullptr);
-        spmv(0, m_loc0 - 1, 1, nullptr);
+        spmv(0, 0, 1);
+        spmv(0, m_loc0 - 1, 1);
         s->ktimer.end(kFusedSpmv);
     } else {
         halo(c, s->z);
         for (size_t si = 0; si < c->slabs.size(); ++si) {
             s->ktimer.begin(kFusedSpmv);
-            leaves[si] = spmv(si, 0, 0, single ? &fin2 : nullptr);
+            leaves[si] = spmv(si, 0, 0);
             s->ktimer.end(kFusedSpmv);
         }
     }
-    if (!fin2.used) reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true, &leaves);
+    reduce<T>(c, 1, kOpIlSpmv, S, nullptr, true, &leaves);
     s->timer.end(kFusedSpmv);
 }
 

@@ -311,8 +311,7 @@ template <typename T, bool Fast, int D, int MINB>
 __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     k_fused_spmv_pair2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves,
-                      const FinishDev<T> fin) {
+                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
     using A = Ar<T, Fast>;
     using P = Pair<T>;
     constexpr int NT = 32 * kStencilWarps, NS = D + 1;
@@ -423,7 +422,6 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         __syncthreads();
         if (threadIdx.y == 0)
             pair_node_sums<T, 2 * NT>(red, stage, nleaves, il, m);
-        if (fin.op >= 0) cta_finish(fin, stage, nleaves, 1, red, tid, NT);
         return;
     }
     *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};

@@ -6,8 +6,8 @@ k_thomas (z' in global memory: n_z*s > 1 KiB); K2 = k_fused_spmv_pair2 (fp64) /
 k_fused_spmv_pair (fp32) for even m, k_fused_spmv_tile for odd m; reduction
 stage 2 = k_tree2_wide / k_tree2_shfl / k_tree2 by leaf count. The worker
 (tests/variant_worker.py) runs shapes that reach each of them, in one process
-per launch-mode setting: the default, programmatic dependent launch off
-(ACG_PDL=0), and the sweep's last CTA finishing the reduction (ACG_CTA_FINISH=1).
+per launch-mode setting: the default and programmatic dependent launch off
+(ACG_PDL=0).
 """
 import os
 import subprocess
@@ -21,7 +21,6 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 VARIANTS = {
     "default": {},
     "no_pdl": {"ACG_PDL": "0"},
-    "cta_finish": {"ACG_CTA_FINISH": "1"},  # last CTA finishes the reduction
 }
 
 

@@ -1,6 +1,6 @@
 """Worker for tests/test_variants.py: one process per kernel-variant setting.
 
-The launch-mode switches (ACG_PDL, ACG_CTA_FINISH) are read once per process,
+The launch-mode switch ACG_PDL is read once per process,
 so each setting runs in its own process. It runs the fused sweeps, apply,
 precondition and two full solves (fp64 and fp32, over SHAPES) and compares them bit for bit with the CPU oracle.
 Prints VARIANT_OK or the first mismatch.
