@@ -3,7 +3,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 for c in c1 c2 c3 c4 c5; do
-  timeout 600 python bench.py --config $c --steps 30 --warmup 3 --no-cpu > gpurun_out/cfg_$c.json 2> gpurun_out/cfg_$c.err
+  timeout 600 python bench.py --config $c --steps ${STEPS:-100} --warmup 20 --no-cpu --sustain-steps 0 > gpurun_out/cfg_$c.json 2> gpurun_out/cfg_$c.err
   python - "$c" <<'PY'
 import json, sys
 c = sys.argv[1]
