@@ -45,14 +45,24 @@ OMEGA2, H = 6.71e-4, 1e-2
 
 
 def cpu_model():
+    """/proc/cpuinfo model name plus family/model numbers (virtualised hosts often
+    report only a generic name)."""
+    info = {}
     try:
         with open("/proc/cpuinfo") as fh:
             for line in fh:
-                if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
+                k, _, v = line.partition(":")
+                k = k.strip()
+                if k in ("model name", "cpu family", "model") and k not in info:
+                    info[k] = v.strip()
+                if not line.strip() and info:
+                    break
     except OSError:
         pass
-    return "unknown"
+    name = info.get("model name", "unknown")
+    if "cpu family" in info and "model" in info:
+        name += f" (family {info['cpu family']}, model {info['model']})"
+    return name
 
 
 def reexec_under_torchrun(n):
