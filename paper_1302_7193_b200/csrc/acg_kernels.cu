@@ -1144,10 +1144,12 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
     post_launch("precondition");
 }
 
-// K2 kernel choice (measured): two adjacent columns per thread
-// for even m — fp64 k_fused_spmv_pair2 (every stencil input in a 3-level
-// cp.async ring, C3 K2 1.18 ms), fp32 k_fused_spmv_pair (neighbour rows loaded
-// a level ahead, C4 K2 2.49 ms); k_fused_spmv_tile (shared z tiles) for odd m.
+// K2 kernel choice (measured): fp64 with even m
+// k_fused_spmv_pair2 (two columns per thread, every stencil input in a 3-level
+// cp.async ring, C3 K2 1.18 ms); fp32 with m % 4 == 0 k_fused_spmv_quad (four
+// columns per thread, the same ring with 16-byte quads, C4 K2 2.37 ms), other
+// even m k_fused_spmv_pair (neighbour rows loaded a level ahead); odd m
+// k_fused_spmv_tile (shared z tiles).
 // Measured-slower kernels (one column per thread with plain or ring loads) and
 // the other ring depths were removed after round 1.
 inline bool spmv_pairs(int m) { return m % 2 == 0; }
@@ -1159,8 +1161,8 @@ bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
         const char* e = std::getenv("ACG_FUSED_HALO");
         return e && std::string(e) == "0";
     }();
-    // producer: k_thomas_tm2 (fp32) or k_thomas_tm (fp64); consumer: k_fused_spmv_pair
-    // (fp32) or k_fused_spmv_pair2 (fp64)
+    // producer: k_thomas_tm2 (fp32) or k_thomas_tm (fp64); consumer: k_fused_spmv_quad /
+    // k_fused_spmv_pair (fp32) or k_fused_spmv_pair2 (fp64)
     const unsigned cols = thomas_tm_cols(v.n_z, sizeof(T));
     const bool k1 = sizeof(T) == 4 ? 2 * cols <= 512 : cols <= 256;
     return !off && v.tm_ok && !phi_in_hbm && k1 && spmv_pairs(v.m);
@@ -1189,7 +1191,30 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
         leaves = fused_leaves(v, narrow ? v.m : kCols, stage);
         T* stg = leaves ? stage : nullptr;
         const dim3 g2((v.m + kCols - 1) / kCols, v.plane_count ? v.plane_count : v.m_loc);
-        if (sizeof(T) == 4) {
+        if constexpr (sizeof(T) == 4) {
+            if (v.m % 4 == 0) {  // four columns per thread (k_fused_spmv_quad)
+                constexpr int kQ = 4 * 32 * kStencilWarps;
+                const bool nq = v.m < kQ && v.m >= 64 && (v.m & (v.m - 1)) == 0;
+                leaves = fused_leaves(v, nq ? v.m : kQ, stage);
+                T* stq = leaves ? stage : nullptr;
+                const dim3 g4((v.m + kQ - 1) / kQ, v.plane_count ? v.plane_count : v.m_loc);
+                // ring depth 3 (one 8-warp CTA per SM: 112 KB of ring); C4 K2 2.374 ms =
+                // 6.37 TB/s vs 2.512 ms for k_fused_spmv_pair; depth 2 with two CTAs: 2.60 ms
+                constexpr int D = 3;
+                const size_t smem = static_cast<size_t>((4 * v.n_z + 3) & ~3) * sizeof(T) +
+                                    static_cast<size_t>(D + 1) * 7 * 32 * kStencilWarps * 16;
+                if (fast) {
+                    ensure_smem(k_fused_spmv_quad<true, D, 1>, smem);
+                    launch_pdl(k_fused_spmv_quad<true, D, 1>, g4, block, smem, st, v, u, p, q, z,
+                               part, S, stq, leaves);
+                } else {
+                    ensure_smem(k_fused_spmv_quad<false, D, 1>, smem);
+                    launch_pdl(k_fused_spmv_quad<false, D, 1>, g4, block, smem, st, v, u, p, q, z,
+                               part, S, stq, leaves);
+                }
+                post_launch("fused_spmv");
+                return leaves;
+            }
             // ring depth 2 (exact: at least 3 CTAs per SM)
             constexpr int D = 2;
             const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +

@@ -426,3 +426,156 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     }
     *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};
 }
+
+// K2 for fp32 with four adjacent columns per thread (m a multiple of 4): every
+// stream moves as one 16-byte quad, so the fp32 sweep issues one cp.async per
+// 16 bytes like the fp64 pair kernel (k_fused_spmv_pair2), and every stencil
+// input — p, q, u, z(k+1), the i+-1 rows and z(j-1), z(j+4) — goes through a
+// D-level cp.async ring (the fp32 pair kernel loads the neighbour rows one
+// level ahead into registers, which leaves their L2 latency exposed).
+// CTA = one i-plane x 1024 j. Columns j+1..j+3's south and j..j+2's north
+// neighbours are lanes of the quad; the arithmetic and association are those
+// of the other K2 kernels (bit-identical).
+struct alignas(16) Quad {
+    float x, y, z, w;
+};
+
+__device__ __forceinline__ void cpa_quad(Quad* sdst, const float* gsrc) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+template <bool Fast, int D, int MINB>
+__global__ void __launch_bounds__(32 * kStencilWarps, MINB)
+    k_fused_spmv_quad(const SlabView<float> v, float* __restrict__ u, float* __restrict__ p,
+                      float* __restrict__ q, const float* __restrict__ z,
+                      float* __restrict__ part, const Scalars<float>* __restrict__ S,
+                      float* __restrict__ stage, int nleaves) {
+    using T = float;
+    using A = Ar<T, Fast>;
+    constexpr int NT = 32 * kStencilWarps, NS = D + 1, CW = 4 * NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* prof = reinterpret_cast<T*>(smem_raw);
+    const int n_z = v.n_z, m = v.m;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    load_profile(prof, v.prof, 4 * n_z, tid, NT);  // static data: before the dependency wait
+    __syncthreads();
+    pdl_wait();
+    if (ld_dep(&S->done)) return;  // block-uniform
+    int il = v.plane_begin + blockIdx.y;
+    if (v.halo.on) {  // fused halo: boundary planes last, after the neighbours' K1 put them
+        const int y = blockIdx.y, ml = v.m_loc;
+        if (ml >= 3) il = y < ml - 2 ? y + 1 : (y == ml - 2 ? 0 : ml - 1);
+        if (il == 0 && v.halo.ghost[0] != nullptr) halo_acquire(v.halo.wait_flag[0], v.halo.seq);
+        if (il == ml - 1 && v.halo.ghost[1] != nullptr) halo_acquire(v.halo.wait_flag[1], v.halo.seq);
+    }
+    const int jr = blockIdx.x * CW + 4 * tid;
+    const bool valid = jr < m;  // m % 4 == 0: all four columns exist
+    if (stage == nullptr && !valid) return;
+    const int j = valid ? jr : m - 4;
+    // profile 4 n_z floats, then the ring [slot][7][NT] quads (16-byte aligned)
+    Quad* ring = reinterpret_cast<Quad*>(prof + ((4 * n_z + 3) & ~3)) + tid;
+    const T* sP = prof + kProfS * n_z;
+    const T* bP = prof + kProfB * n_z;
+    const T* cP = prof + kProfC * n_z;
+    const T* dP = prof + kProfD * n_z;
+    T sig[4] = {T(0), T(0), T(0), T(0)};
+    if (valid) {  // the idle warps of a narrow panel's CTA (fused reduction) skip the sweep
+        Col<T> cc[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) cc[t] = load_col(v, il, j + t);
+        const T alpha = ld_dep(&S->alpha), beta = ld_dep(&S->beta);
+        const long long base = static_cast<long long>(il) * v.plane + j;
+        const T* zc = z + base;
+        T* uc = u + base;
+        T* pc = p + base;
+        T* qc = q + base;
+        const long long sm = m;
+        long long oe = cc[0].oe, ow = cc[0].ow;  // same for all four columns (same plane)
+        if (v.halo.on) {  // ghost rows straight from this rank's mailbox
+            if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
+            if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
+        }
+        auto issue = [&](int k, int s) {
+            const long long l = static_cast<long long>(k) * sm;
+            Quad* r0 = ring + s * 7 * NT;
+            cpa_quad(r0, pc + l);
+            cpa_quad(r0 + NT, qc + l);
+            cpa_quad(r0 + 2 * NT, uc + l);
+            if (k + 1 < n_z) cpa_quad(r0 + 3 * NT, zc + l + sm);
+            cpa_quad(r0 + 4 * NT, zc + l + oe);
+            cpa_quad(r0 + 5 * NT, zc + l + ow);
+            T* e = reinterpret_cast<T*>(r0 + 6 * NT);  // z(j-1), z(j+4) (own values on the edges)
+            cpa(e, zc + l + cc[0].os);
+            cpa(e + 1, zc + l + 3 + cc[3].on);
+        };
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            if (t < n_z) issue(t, t);
+            cp_commit();
+        }
+        Quad z0 = *reinterpret_cast<const Quad*>(zc), zd = z0;
+        int cs = 0, ps_ = D;
+        for (int k = 0; k < n_z; ++k) {
+            const long long l = static_cast<long long>(k) * sm;
+            cp_wait<D - 1>();
+            const Quad* r0 = ring + cs * 7 * NT;
+            const Quad pq = r0[0], qq = r0[NT], uq = r0[2 * NT];
+            const Quad zu = k + 1 < n_z ? r0[3 * NT] : z0;
+            const Quad ce = r0[4 * NT], cw = r0[5 * NT];
+            const T* ex = reinterpret_cast<const T*>(r0 + 6 * NT);
+            const T zs0 = ex[0], zn3 = ex[1];
+            if (k + D < n_z) issue(k + D, ps_);
+            cp_commit();
+            cs = cs + 1 == NS ? 0 : cs + 1;
+            ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
+            const T P0[4] = {pq.x, pq.y, pq.z, pq.w}, Q0[4] = {qq.x, qq.y, qq.z, qq.w};
+            const T U0[4] = {uq.x, uq.y, uq.z, uq.w}, Z0[4] = {z0.x, z0.y, z0.z, z0.w};
+            const T ZU[4] = {zu.x, zu.y, zu.z, zu.w}, ZD[4] = {zd.x, zd.y, zd.z, zd.w};
+            const T ZE[4] = {ce.x, ce.y, ce.z, ce.w}, ZW[4] = {cw.x, cw.y, cw.z, cw.w};
+            T un[4], pn[4], qn[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                un[t] = A::add(U0[t], A::mul(alpha, P0[t]));
+                pn[t] = A::add(A::mul(beta, P0[t]), Z0[t]);
+                const T qb = A::mul(beta, Q0[t]);
+                const T zn = t < 3 ? Z0[t + 1] : zn3;  // north: the next lane, z(j+4) at the end
+                const T zs = t > 0 ? Z0[t - 1] : zs0;  // south: the previous lane, z(j-1) first
+                const Col<T>& c = cc[t];
+                const T dq = stencil<T, Fast>(sP[k], c.area, c.adiag, bP[k], cP[k], c.ae, c.aw,
+                                              c.an, c.as, Z0[t], ZU[t], ZD[t], ZE[t], ZW[t], zn, zs);
+                qn[t] = A::add(qb, A::mul(dP[k], dq));
+                sig[t] = A::add(sig[t], A::mul(pn[t], qn[t]));
+            }
+            __stcs(reinterpret_cast<float4*>(uc + l), make_float4(un[0], un[1], un[2], un[3]));
+            __stcs(reinterpret_cast<float4*>(pc + l), make_float4(pn[0], pn[1], pn[2], pn[3]));
+            __stcs(reinterpret_cast<float4*>(qc + l), make_float4(qn[0], qn[1], qn[2], qn[3]));
+            zd = z0;
+            z0 = zu;
+        }
+        cp_wait<0>();
+    }
+    if (stage != nullptr) {  // fused reduction stage 1 (quad_node_sums)
+        __syncthreads();
+        T* red = prof + ((4 * n_z + 3) & ~3);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) red[4 * tid + t] = sig[t];
+        __syncthreads();
+        if (threadIdx.y == 0) {
+            if (m >= CW) {
+                cta_subtree_sums<T, CW>(red, 1, stage, nleaves,
+                                        (static_cast<long long>(il) * m + blockIdx.x * CW) / CW);
+            } else {
+                switch (m) {  // narrower power-of-two panel: the node is the whole plane
+                    case 512: cta_subtree_sums<T, 512>(red, 1, stage, nleaves, il); break;
+                    case 256: cta_subtree_sums<T, 256>(red, 1, stage, nleaves, il); break;
+                    case 128: cta_subtree_sums<T, 128>(red, 1, stage, nleaves, il); break;
+                    default: cta_subtree_sums<T, 64>(red, 1, stage, nleaves, il); break;
+                }
+            }
+        }
+        return;
+    }
+    *reinterpret_cast<float4*>(part + static_cast<long long>(il) * m + j) =
+        make_float4(sig[0], sig[1], sig[2], sig[3]);
+}

@@ -2,8 +2,9 @@
 
 Kernel choice is by shape and precision (no tuning switches since round 2):
 K1 = k_thomas_tm (fp64, and fp32 with odd m) / k_thomas_tm2 (fp32, even m) /
-k_thomas (z' in global memory: n_z*s > 1 KiB); K2 = k_fused_spmv_pair2 (fp64) /
-k_fused_spmv_pair (fp32) for even m, k_fused_spmv_tile for odd m; reduction
+k_thomas (z' in global memory: n_z*s > 1 KiB); K2 = k_fused_spmv_pair2 (fp64,
+even m) / k_fused_spmv_quad (fp32, m % 4 == 0) / k_fused_spmv_pair (fp32, other
+even m), k_fused_spmv_tile for odd m; reduction
 stage 2 = k_tree2_wide / k_tree2_shfl / k_tree2 by leaf count. The worker
 (tests/variant_worker.py) runs shapes that reach each of them, in one process
 per launch-mode setting: the default and programmatic dependent launch off
