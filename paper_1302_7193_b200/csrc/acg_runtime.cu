@@ -10,6 +10,7 @@
 #include <fcntl.h>
 #include <unistd.h>
 #include <nccl.h>  // types only; NCCL itself is dlopen'ed on first use
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops without a profiler
 
 #include <algorithm>
 #include <chrono>
@@ -355,6 +356,13 @@ struct acg_field {
 };
 
 namespace {
+
+// NVTX range for profilers (nsys/ncu timelines): init sweeps, iteration
+// batches, finish, CSR assembly.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct CtxLock {
     std::unique_lock<std::recursive_mutex> lk;
@@ -1171,6 +1179,7 @@ void op_copy(const acg_context* c, const acg_field* x, acg_field* y, const std::
 // for `layout`, csr.hpp:92-124) and kept until release_scratch.
 template <typename T>
 void ensure_csr(const acg_context* cc, int layout) {
+    NvtxRange nr("acg csr assemble");
     acg_context* c = const_cast<acg_context*>(cc);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         Slab& s = c->slabs[si];
@@ -1736,6 +1745,7 @@ acg_solver* cached_solver(const acg_context* c, const acg_solver_config* cfg) {
 
 template <typename T>
 void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
+    NvtxRange nr("acg solve init");
     const acg_context* c = s->ctx;
     s->t0 = std::chrono::steady_clock::now();
     s->launches0 = g_launches.load();
@@ -2057,6 +2067,7 @@ void drain_histories(acg_solver* s, const int counts[4]) {
 // current one (pipelined, so the GPU never idles on the host).
 template <typename T>
 void solver_run(acg_solver* s) {
+    NvtxRange nr("acg iterations");
     const acg_context* c = s->ctx;
     const double est_us = std::max(2.0, bytes_per_iteration(c) / 4.0e3);
     int batch = static_cast<int>(std::ceil(1500.0 / est_us));
@@ -2095,6 +2106,7 @@ void solver_run(acg_solver* s) {
 template <typename T>
 void solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* res, double* hr, double* hk,
                    double* ha, double* hb) {
+    NvtxRange nr("acg solve finish");
     const acg_context* c = s->ctx;
     auto S = sv<T>(s);
     CK(cudaStreamSynchronize(c->stream));
