@@ -40,6 +40,8 @@ CONFIGS = {
     "c3": dict(m=1024, n_z=128, dtype="f64", lambda2=3.32e-2),
     "c4": dict(m=2048, n_z=128, dtype="f32", lambda2=1.0e2),  # median gamma^2 ~ 1e4
     "c5": dict(m=4096, n_z=64, dtype="f64", lambda2=3.32e-2),
+    # not a BASELINE config: columns taller than two CTAs' TMEM (z' in 512 columns)
+    "tall": dict(m=1024, n_z=256, dtype="f64", lambda2=3.32e-2),
 }
 OMEGA2, H = 6.71e-4, 1e-2
 

@@ -1056,8 +1056,10 @@ int launch_thomas_tm2_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2
 //    half the bytes per instruction); needs even m;
 //  * fp64, and fp32 with odd m: k_thomas_tm, one column per thread, z' in TMEM
 //    (C3: 0.78 ms; two columns per thread 0.99 ms);
+//  * columns whose z' needs all 512 TMEM columns (fp64 128 < n_z <= 256) run
+//    k_thomas_tm with one CTA per SM (1024^2 x 256: K1 2.10 vs 3.55 ms);
 //  * k_thomas (z' through global memory) when the TMEM sweep cannot run: n_z*s
-//    above 1 KiB, or division operand ranges that fail k_validate_tm.
+//    above 2 KiB, or division operand ranges that fail k_validate_tm.
 // Measured-slower configurations (TMA-fed tiles, other ring depths and CTA
 // shapes, occupancy caps) were removed after round 1; DESIGN.md keeps their numbers.
 using ThomasTmDefault = ThomasTmCfg<4, 15, 15>;
@@ -1072,7 +1074,8 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
                                                                              S, gate, stage, st);
         if (l >= 0) return l;
     }
-    if (tmem && thomas_tm_cols(v.n_z, sizeof(T)) <= 256)
+    // up to 256 columns: two CTAs per SM; 512 (fp64 n_z <= 256, fp32 <= 512): one
+    if (tmem && thomas_tm_cols(v.n_z, sizeof(T)) <= 512)
         return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmDefault>(v, r, in, out, p2, pk, S, gate,
                                                                     stage, st);
     if (v.halo.on) {  // fused_halo_ok admits only the TMEM sweeps
@@ -1164,7 +1167,7 @@ bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
     // producer: k_thomas_tm2 (fp32) or k_thomas_tm (fp64); consumer: k_fused_spmv_quad /
     // k_fused_spmv_pair (fp32) or k_fused_spmv_pair2 (fp64)
     const unsigned cols = thomas_tm_cols(v.n_z, sizeof(T));
-    const bool k1 = sizeof(T) == 4 ? 2 * cols <= 512 : cols <= 256;
+    const bool k1 = sizeof(T) == 4 ? 2 * cols <= 512 : cols <= 512;
     return !off && v.tm_ok && !phi_in_hbm && k1 && spmv_pairs(v.m);
 }
 

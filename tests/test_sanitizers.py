@@ -49,11 +49,11 @@ def keep_log(name, text):
 # Missing init." at shared address 0 and then aborts it — also a kernel that
 # only allocates, relinquishes and frees TMEM (scripts/micro/tmem_synccheck.cu,
 # test_synccheck_rejects_bare_tmem_alloc below). So synccheck runs on shapes
-# whose sweeps do not use tensor memory: fp64 columns taller than TMEM holds
-# (k_thomas) with even m (k_fused_spmv_pair2) and odd m (k_fused_spmv_tile),
-# fp32 n_z = 300 (k_thomas, k_fused_spmv_pair). The TMEM kernels are covered by
-# memcheck, racecheck and initcheck.
-NO_TMEM = ["32x160:f64", "33x160:f64", "16x300:f32"]
+# whose sweeps do not use tensor memory: columns taller than an SM's TMEM holds
+# (fp64 n_z > 256, fp32 n_z > 512: k_thomas) with even m (k_fused_spmv_pair2,
+# k_fused_spmv_quad) and odd m (k_fused_spmv_tile). The TMEM kernels are
+# covered by memcheck, racecheck and initcheck.
+NO_TMEM = ["32x272:f64", "33x272:f64", "16x520:f32"]
 # every other tool: the TMEM sweeps with the fused reduction (power-of-two
 # column counts: K1 tree nodes of 128 columns, K2 of a whole narrow plane),
 # a ragged odd panel (k_fused_spmv_tile, k_tree1) — small, the tools are slow
@@ -78,7 +78,7 @@ def test_single_process_clean(tool):
 def test_two_rank_peer_memory_clean(tool):
     # synccheck: tall columns keep the sweeps off tensor memory (see NO_TMEM); the
     # peer-memory halo then runs as copy + signal/wait kernels
-    shape = ["64", "160"] if tool == "synccheck" else ["64", "24"]
+    shape = ["64", "272"] if tool == "synccheck" else ["64", "24"]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(29640 + TOOLS.index(tool)),
            "--no-python", sanitizer(), "--tool", tool, "--error-exitcode", "97",

@@ -54,10 +54,12 @@ def check(m, n_z, dtype):
     return None
 
 
-# (m, n_z) reaching every shipped kernel: even / ragged widths (pair kernels,
-# TMEM sweeps), odd m (k_fused_spmv_tile; k_thomas_tm for fp32), fp64 columns
-# taller than TMEM holds (k_thomas, z' in global memory), fp32 ones too (n_z 300)
-SHAPES = ((128, 24), (66, 19), (65, 12), (32, 160), (16, 300))
+# (m, n_z) reaching every shipped kernel: even / ragged widths (pair and quad
+# kernels, TMEM sweeps), odd m (k_fused_spmv_tile; k_thomas_tm for fp32), fp64
+# columns whose z' needs all 512 TMEM columns (one CTA per SM: n_z 160), and
+# columns taller than TMEM holds (k_thomas, z' in global memory: fp64 n_z 272,
+# fp32 n_z 520)
+SHAPES = ((128, 24), (66, 19), (65, 12), (32, 160), (16, 272), (8, 520))
 
 
 def main():
