@@ -127,3 +127,36 @@ def test_host_assemble_csr_matches_reference_module(acg):
         e_rp, e_ci, e_va = ref[f"{m}_{nz}_{sph}"]
         assert rp.tolist() == e_rp and ci.tolist() == e_ci
         assert [float(x).hex() for x in va] == e_va
+
+
+def test_matrix_free_vs_csr_agree(acg):
+    """test_solver.cpp:136-149: the two backends' standard-loop residual histories
+    agree to 1e-13 * ||r0|| (different summation orders, same operator)."""
+    prob = Problem(16, 32)
+    ctx = ctx_for(acg, prob)
+    f = acg.random_field(16, 32, 42)
+    kw = dict(epsilon=1e-300, tau=1e-300, maxiter=50, variant="standard")
+    _, rm = acg.solve(ctx, f, backend="matrix-free", **kw)
+    _, rc = acg.solve(ctx, f, backend="csr", **kw)
+    r0 = rm.residual_history[0]
+    assert len(rm.residual_history) == len(rc.residual_history)
+    assert np.abs(rm.residual_history - rc.residual_history).max() <= 1e-13 * r0
+
+
+def test_csr_breakdown_message(acg):
+    """A non-SPD operator (d negated, test_solver.cpp:194-204) on the CSR backend
+    raises NumericalBreakdown with the reference's message where the reference's
+    CsrBackend raises it (oracle/_ref run live)."""
+    from oracle.oracle import Oracle
+    from paper_1302_7193_b200 import capi
+    prob = Problem(4, 8)
+    o = Oracle(prob).flip_d()
+    cctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag)
+    f = o.random_field(3)
+    ff = cctx.field().upload(f)
+    with pytest.raises(capi.BreakdownError) as ei:
+        capi.solve(cctx, ff, variant=capi.STANDARD, backend=capi.CSR)
+    if ref_available():
+        with pytest.raises(RuntimeError) as er:
+            Reference(prob, flip_d=True).solve(f, variant="standard", backend="csr")
+        assert str(er.value).split(":")[0] in str(ei.value)
