@@ -140,6 +140,10 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # wait for the first sample (taken before the timed region, not counted):
+            # nvidia-smi's start-up (process launch, NVML init) then stays outside the
+            # timed region, which matters for sub-millisecond regions (small grids)
+            self.proc.stdout.readline()
         except Exception:
             self.proc = None
         return self
