@@ -143,7 +143,9 @@ class ClockSampler:
             # wait for the first sample (taken before the timed region, not counted):
             # nvidia-smi's start-up (process launch, NVML init) then stays outside the
             # timed region, which matters for sub-millisecond regions (small grids)
-            self.proc.stdout.readline()
+            import select
+            if select.select([self.proc.stdout], [], [], 5.0)[0]:
+                self.proc.stdout.readline()
         except Exception:
             self.proc = None
         return self
