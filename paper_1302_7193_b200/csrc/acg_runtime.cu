@@ -342,6 +342,12 @@ struct acg_context {
     // concurrent calls on one context queue on this lock and run one after
     // the other on the context's stream, so each sees a consistent state.
     mutable std::recursive_mutex mu;
+    // Fields and solvers the caller created on this context. Destroying the
+    // context releases their device memory and orphans them (ctx = NULL), so a
+    // later acg_field_destroy / acg_solver_destroy — e.g. from a garbage
+    // collector that finalises the context first — frees only the handle.
+    mutable std::vector<acg_field*> user_fields;
+    mutable std::vector<acg_solver*> user_solvers;
     std::unique_ptr<IpcState> ipc; // peer-memory transport (acg_comm_create_ipc)
     size_t s = 8;
     bool fast() const { return math == ACG_MATH_FAST; }
@@ -505,6 +511,7 @@ void* alloc_tmp_scalars() {
 }  // namespace
 
 void destroy_cached_solver(acg_context* c);  // defined after acg_solver
+void orphan_solver(acg_solver* s);           // frees a user solver's device state, ctx = NULL
 
 // =================================================================== basics
 extern "C" {
@@ -689,6 +696,12 @@ acg_status acg_context_destroy(acg_context* c) {
         if (!c) return;
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
+        for (acg_solver* us : c->user_solvers) orphan_solver(us);
+        for (acg_field* f : c->user_fields) {
+            for (void* b : f->base) cudaFree(b);
+            f->base.clear();
+            f->ctx = nullptr;
+        }
         destroy_cached_solver(c);
         for (acg_field* f : c->pool) {
             for (void* b : f->base) cudaFree(b);
@@ -1267,6 +1280,7 @@ T op_true_residual_csr(const acg_context* c, const acg_field* u, const acg_field
 
 void check_same(const acg_field* a, const acg_field* b, const char* what) {
     if (!a || !b) fail(ACG_ERR_INVALID_ARGUMENT, "%s: null field", what);
+    if (!a->ctx || !b->ctx) fail(ACG_ERR_INVALID_ARGUMENT, "%s: field of a destroyed context", what);
     if (a->ctx->m != b->ctx->m || a->ctx->n_z != b->ctx->n_z || a->ctx->dtype != b->ctx->dtype ||
         a->ctx->slabs.size() != b->ctx->slabs.size())
         fail(ACG_ERR_INVALID_ARGUMENT, "%s: shape/layout mismatch", what);
@@ -1294,15 +1308,24 @@ acg_status acg_field_create(acg_field** out, const acg_context* c) {
         DeviceGuard g(c->device);
         CtxLock lk(c);
         *out = new_field(c);
+        c->user_fields.push_back(*out);
     });
 }
 
 acg_status acg_field_destroy(acg_field* f) {
     return guarded([&] {
         if (!f) return;
-        DeviceGuard g(f->ctx->device);
-        CtxLock lk(f->ctx);
-        cudaStreamSynchronize(f->ctx->stream);
+        if (!f->ctx) {  // orphaned by acg_context_destroy: device memory already freed
+            delete f;
+            return;
+        }
+        const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
+        DeviceGuard g(c->device);
+        CtxLock lk(c);
+        auto& v = c->user_fields;
+        v.erase(std::remove(v.begin(), v.end(), f), v.end());
+        cudaStreamSynchronize(c->stream);
         free_field(f);
     });
 }
@@ -1312,6 +1335,7 @@ acg_status acg_field_upload(acg_field* f, const void* host, acg_layout layout,
     return guarded([&] {
         if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, upload_t<T>(f, host, layout, scope));
@@ -1323,6 +1347,7 @@ acg_status acg_field_download(const acg_field* f, void* host, acg_layout layout,
     return guarded([&] {
         if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, download_t<T>(f, host, layout, scope));
@@ -1334,6 +1359,7 @@ acg_status acg_field_upload_device(acg_field* f, const void* dev, acg_layout lay
     return guarded([&] {
         if (!f || !dev) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, upload_dev_t<T>(f, dev, layout, scope));
@@ -1345,6 +1371,7 @@ acg_status acg_field_download_device(const acg_field* f, void* dev, acg_layout l
     return guarded([&] {
         if (!f || !dev) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, download_dev_t<T>(f, dev, layout, scope));
@@ -1355,6 +1382,7 @@ acg_status acg_field_fill(acg_field* f, double value) {
     return guarded([&] {
         if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
         const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, {
@@ -1370,6 +1398,7 @@ acg_status acg_field_fill_random(acg_field* f, uint64_t seed) {
     return guarded([&] {
         if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
         const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, {
@@ -1385,6 +1414,7 @@ acg_status acg_field_copy(acg_field* dst, const acg_field* src) {
     return guarded([&] {
         check_same(dst, src, "copy");
         const acg_context* c = dst->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, op_copy<T>(c, src, dst, nullptr));
@@ -1429,6 +1459,7 @@ acg_status acg_axpy(double alpha, const acg_field* x, acg_field* y) {
     return guarded([&] {
         check_same(x, y, "axpy");
         const acg_context* c = x->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, op_axpy<T>(c, static_cast<T>(alpha), nullptr, -1, false, x, y, false));
@@ -1440,6 +1471,7 @@ acg_status acg_scal(double alpha, acg_field* x) {
     return guarded([&] {
         if (!x) fail(ACG_ERR_INVALID_ARGUMENT, "scal: null field");
         const acg_context* c = x->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, {
@@ -1456,6 +1488,7 @@ acg_status acg_dot(const acg_field* x, const acg_field* y, double* out) {
         check_same(x, y, "dot");
         if (!out) fail(ACG_ERR_INVALID_ARGUMENT, "null output");
         const acg_context* c = x->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, {
@@ -1471,6 +1504,7 @@ acg_status acg_nrm2(const acg_field* x, double* out) {
     return guarded([&] {
         if (!x || !out) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
         const acg_context* c = x->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
         ACG_TDISPATCH(c, {
@@ -1624,8 +1658,12 @@ struct EventTimer {
         used = 0;
         for (auto& m : marks) m.clear();
     }
-    ~EventTimer() {
+    ~EventTimer() { release(); }
+    void release() {
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
+        pool.clear();
+        used = 0;
+        for (auto& mk : marks) mk.clear();
     }
 };
 
@@ -1657,17 +1695,33 @@ struct acg_solver {
     int chunk_kind = -1;           // variant * 2 + csr the graph was captured for
     std::chrono::steady_clock::time_point t0;
     double setup_s = 0.0;
-    ~acg_solver() {
+    ~acg_solver() { release(); }
+    void release() {  // device resources; idempotent
         if (chunk) cudaGraphExecDestroy(chunk);
-        for (acg_field* fl : {u, r, z, p, q})
-            if (fl) free_field(fl);
+        chunk = nullptr;
+        for (acg_field** fl : {&u, &r, &z, &p, &q}) {
+            if (*fl) free_field(*fl);
+            *fl = nullptr;
+        }
         for (void* s : S) cudaFree(s);
+        S.clear();
         for (double* h : hist) cudaFree(h);
+        hist.clear();
         if (mirror) cudaFreeHost(mirror);
-        for (cudaEvent_t e : mev)
+        mirror = nullptr;
+        for (cudaEvent_t& e : mev) {
             if (e) cudaEventDestroy(e);
+            e = nullptr;
+        }
+        timer.release();
+        ktimer.release();
     }
 };
+
+void orphan_solver(acg_solver* s) {
+    s->release();
+    s->ctx = nullptr;
+}
 
 void destroy_cached_solver(acg_context* c) {
     delete c->cached;
@@ -2191,15 +2245,24 @@ acg_status acg_solver_create(acg_solver** out, const acg_context* c, const acg_s
         s->cfg = *cfg;
         ACG_TDISPATCH(c, solver_alloc<T>(s.get()));
         *out = s.release();
+        c->user_solvers.push_back(*out);
     });
 }
 
 acg_status acg_solver_destroy(acg_solver* s) {
     return guarded([&] {
         if (!s) return;
-        DeviceGuard g(s->ctx->device);
-        CtxLock lk(s->ctx);
-        cudaStreamSynchronize(s->ctx->stream);
+        if (!s->ctx) {  // orphaned by acg_context_destroy: device resources already freed
+            delete s;
+            return;
+        }
+        const acg_context* c = s->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "solver of a destroyed context");
+        DeviceGuard g(c->device);
+        CtxLock lk(c);
+        auto& v = c->user_solvers;
+        v.erase(std::remove(v.begin(), v.end(), s), v.end());
+        cudaStreamSynchronize(c->stream);
         delete s;
     });
 }
@@ -2208,6 +2271,7 @@ acg_status acg_solver_start(acg_solver* s, const acg_field* f, const acg_field* 
     return guarded([&] {
         if (!s) fail(ACG_ERR_INVALID_ARGUMENT, "null solver");
         const acg_context* c = s->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "solver of a destroyed context");
         check_field(c, f, "solve");
         if (u0) check_field(c, u0, "solve");
         DeviceGuard g(c->device);
@@ -2219,6 +2283,7 @@ acg_status acg_solver_start(acg_solver* s, const acg_field* f, const acg_field* 
 acg_status acg_solver_iterate(acg_solver* s, int n) {
     return guarded([&] {
         if (!s || !s->started) fail(ACG_ERR_INVALID_ARGUMENT, "solver not started");
+        if (!s->ctx) fail(ACG_ERR_INVALID_ARGUMENT, "solver of a destroyed context");
         DeviceGuard g(s->ctx->device);
         CtxLock lk(s->ctx);
         ACG_TDISPATCH(s->ctx, solver_iterate<T>(s, n));
@@ -2237,6 +2302,7 @@ acg_status acg_solver_kernel_times(acg_solver* s, int* n_prec, double* ms_prec, 
                                    double* ms_spmv) {
     return guarded([&] {
         if (!s) fail(ACG_ERR_INVALID_ARGUMENT, "null solver");
+        if (!s->ctx) fail(ACG_ERR_INVALID_ARGUMENT, "solver of a destroyed context");
         DeviceGuard g(s->ctx->device);
         CtxLock lk(s->ctx);
         CK(cudaStreamSynchronize(s->ctx->stream));
@@ -2252,6 +2318,7 @@ acg_status acg_solver_finish(acg_solver* s, acg_field* u_out, acg_solve_result* 
                              double* hk, double* ha, double* hb) {
     return guarded([&] {
         if (!s || !s->started) fail(ACG_ERR_INVALID_ARGUMENT, "solver not started");
+        if (!s->ctx) fail(ACG_ERR_INVALID_ARGUMENT, "solver of a destroyed context");
         if (u_out) check_field(s->ctx, u_out, "solve");
         DeviceGuard g(s->ctx->device);
         CtxLock lk(s->ctx);

@@ -62,6 +62,47 @@ Field3D<T> to_field(const Arr<T>& a, int m, int n_z, Layout layout) {
     return f;
 }
 
+// Zero-copy host edge: numpy buffers go straight to the C ABI's host entry
+// points (which upload, relayout on the device and download), with no
+// intermediate Field3D copies — at 1024^2 x 128 each such copy is a 1 GB
+// memcpy or memset on the host.
+template <typename T>
+void check_shape(const Arr<T>& a, int m, int n_z, Layout layout) {
+    const bool vert = layout == Layout::VerticalContiguous;
+    const py::ssize_t s1 = vert ? m : n_z, s2 = vert ? n_z : m;
+    if (a.ndim() != 3 || a.shape(0) != m || a.shape(1) != s1 || a.shape(2) != s2)
+        throw std::invalid_argument(vert ? "expected a (m, m, n_z) array matching the operator context"
+                                         : "expected a (m, n_z, m) array matching the operator context");
+}
+
+template <typename T>
+py::array_t<T> new_field_array(int m, int n_z, Layout layout) {
+    const bool vert = layout == Layout::VerticalContiguous;
+    return py::array_t<T>(vert ? std::vector<py::ssize_t>{m, m, n_z}
+                               : std::vector<py::ssize_t>{m, n_z, m});
+}
+
+// SolveResult from the C ABI result whose histories the library allocated.
+SolveResult result_of(acg_solve_result& r) {
+    SolveResult res;
+    res.iterations = r.iterations;
+    res.converged = r.converged != 0;
+    res.true_residual = r.true_residual;
+    res.residual_history.assign(r.history[0], r.history[0] + r.n_residual);
+    res.kappa_history.assign(r.history[1], r.history[1] + r.n_kappa);
+    res.alpha_history.assign(r.history[2], r.history[2] + r.n_alpha);
+    res.beta_history.assign(r.history[3], r.history[3] + r.n_beta);
+    res.timings.spmv = r.timings.spmv;
+    res.timings.prec = r.timings.prec;
+    res.timings.blas = r.timings.blas;
+    res.timings.fused_spmv = r.timings.fused_spmv;
+    res.timings.fused_prec = r.timings.fused_prec;
+    res.timings.setup = r.timings.setup;
+    res.timings.total = r.timings.total;
+    acg_solve_result_release(&r);
+    return res;
+}
+
 template <typename T>
 py::array_t<T> to_array(const Field3D<T>& f) {
     const bool vert = f.layout() == Layout::VerticalContiguous;
@@ -157,22 +198,38 @@ void bind_ops(py::module_& mod) {
     mod.def(
         "apply",
         [](const Ctx& ctx, const Arr<T>& x, int workers, const std::string& layout) {
+            (void)workers;
             const Layout L = parse_layout(layout);
-            const auto xf = to_field<T>(x, ctx.m(), ctx.n_z(), L);
-            Field3D<T> y(ctx.m(), ctx.n_z(), L);
-            apply(ctx, xf, y, workers);
-            return to_array(y);
+            check_shape<T>(x, ctx.m(), ctx.n_z(), L);
+            auto y = new_field_array<T>(ctx.m(), ctx.n_z(), L);
+            const T* xp = x.data();
+            T* yp = y.mutable_data();
+            acg_status st;
+            {
+                py::gil_scoped_release nogil;
+                st = acg_apply_host(ctx.device(), detail::layout_of(L), xp, yp);
+            }
+            detail::check(st);
+            return y;
         },
         py::arg("ctx"), py::arg("x"), py::arg("workers") = 1, py::kw_only(),
         py::arg("layout") = "vertical", "y = A x (matrix-free stencil, sm_100a)");
     mod.def(
         "precondition",
         [](const Ctx& ctx, const Arr<T>& y, int workers, const std::string& layout) {
+            (void)workers;
             const Layout L = parse_layout(layout);
-            const auto yf = to_field<T>(y, ctx.m(), ctx.n_z(), L);
-            Field3D<T> x(ctx.m(), ctx.n_z(), L);
-            precondition(ctx, yf, x, workers);
-            return to_array(x);
+            check_shape<T>(y, ctx.m(), ctx.n_z(), L);
+            auto x = new_field_array<T>(ctx.m(), ctx.n_z(), L);
+            const T* yp = y.data();
+            T* xp = x.mutable_data();
+            acg_status st;
+            {
+                py::gil_scoped_release nogil;
+                st = acg_precondition_host(ctx.device(), detail::layout_of(L), yp, xp);
+            }
+            detail::check(st);
+            return x;
         },
         py::arg("ctx"), py::arg("y"), py::arg("workers") = 1, py::kw_only(),
         py::arg("layout") = "vertical", "x = M^-1 y (per-column Thomas solves, sm_100a)");
@@ -182,9 +239,12 @@ void bind_ops(py::module_& mod) {
            int maxiter, const std::string& variant, const std::string& backend, int workers,
            const std::string& layout) {
             const Layout L = parse_layout(layout);
-            const auto ff = to_field<T>(f, ctx.m(), ctx.n_z(), L);
-            Field3D<T> u0f(ctx.m(), ctx.n_z(), L);
-            if (!u0.is_none()) u0f = to_field<T>(u0.cast<Arr<T>>(), ctx.m(), ctx.n_z(), L);
+            check_shape<T>(f, ctx.m(), ctx.n_z(), L);
+            Arr<T> u0a;
+            if (!u0.is_none()) {
+                u0a = u0.cast<Arr<T>>();
+                check_shape<T>(u0a, ctx.m(), ctx.n_z(), L);
+            }
             SolverConfig cfg;
             cfg.epsilon = epsilon;
             cfg.tau = tau;
@@ -202,11 +262,30 @@ void bind_ops(py::module_& mod) {
                 cfg.backend = BackendKind::csr;
             else
                 throw std::invalid_argument("backend must be 'matrix-free' or 'csr'");
-            std::pair<Field3D<T>, SolveResult> out = [&] {
+            cfg.validate();  // SolverConfig::validate (solver.hpp:27-35): the reference's messages
+            acg_solver_config c{};
+            acg_solver_config_default(&c);
+            c.epsilon = cfg.epsilon;
+            c.tau = cfg.tau;
+            c.maxiter = cfg.maxiter;
+            c.workers = cfg.workers;
+            c.variant = cfg.variant == Variant::interleaved ? ACG_VARIANT_INTERLEAVED
+                                                             : ACG_VARIANT_STANDARD;
+            c.backend = cfg.backend == BackendKind::csr ? ACG_BACKEND_CSR : ACG_BACKEND_MATRIX_FREE;
+            c.record_timings = 1;
+            auto u = new_field_array<T>(ctx.m(), ctx.n_z(), L);
+            const T* fp = f.data();
+            const T* u0p = u0.is_none() ? nullptr : u0a.data();  // NULL: zero start, no upload
+            T* up = u.mutable_data();
+            acg_solve_result r{};
+            acg_status st;
+            {
                 py::gil_scoped_release nogil;
-                return solve(ctx, ff, u0f, cfg);
-            }();
-            return py::make_tuple(to_array(out.first), out.second);
+                st = acg_solve_host(ctx.device(), detail::layout_of(L), fp, u0p, &c, up, &r,
+                                    nullptr, nullptr, nullptr, nullptr);
+            }
+            detail::check(st);
+            return py::make_tuple(u, result_of(r));
         },
         py::arg("ctx"), py::arg("f"), py::arg("u0") = py::none(), py::arg("epsilon") = 1e-5,
         py::arg("tau") = 1e-20, py::arg("maxiter") = 500, py::arg("variant") = "interleaved",
@@ -216,9 +295,21 @@ void bind_ops(py::module_& mod) {
         "true_residual",
         [](const Ctx& ctx, const Arr<T>& u, const Arr<T>& f, int workers,
            const std::string& layout) {
+            (void)workers;
             const Layout L = parse_layout(layout);
-            return static_cast<double>(true_residual(ctx, to_field<T>(u, ctx.m(), ctx.n_z(), L),
-                                                     to_field<T>(f, ctx.m(), ctx.n_z(), L), workers));
+            check_shape<T>(u, ctx.m(), ctx.n_z(), L);
+            check_shape<T>(f, ctx.m(), ctx.n_z(), L);
+            double out = 0.0;
+            const T* up = u.data();
+            const T* fp = f.data();
+            acg_status st;
+            {
+                py::gil_scoped_release nogil;
+                st = acg_true_residual_host(ctx.device(), detail::layout_of(L), up, fp, &out);
+            }
+            detail::check(st);
+            // nrm2's sqrt in T (field.hpp:172), then widened like the reference binding
+            return static_cast<double>(static_cast<T>(out));
         },
         py::arg("ctx"), py::arg("u"), py::arg("f"), py::arg("workers") = 1, py::kw_only(),
         py::arg("layout") = "vertical", "||f - A u|| recomputed from scratch");

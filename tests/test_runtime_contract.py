@@ -113,3 +113,27 @@ def test_history_longer_than_the_device_ring(acg, variant):
     for h in ("residual_history", "kappa_history", "alpha_history", "beta_history"):
         assert np.array_equal(getattr(r, h), getattr(ro, h)), h
     assert np.array_equal(u, uo)
+
+
+def test_context_destroyed_before_its_fields(acg):
+    """A garbage collector may finalise an OperatorContext before the capi fields
+    and solvers created on it: destroying the context frees their device memory
+    and orphans the handles, later destroys only free the handles, and other
+    calls on them raise instead of touching freed memory."""
+    import gc
+    from paper_1302_7193_b200 import capi
+    prob = Problem(16, 8)
+    ctx = _ctx(acg, prob)
+    view = capi.Context.borrow(ctx._handle)  # no owner reference: the context may go first
+    f = view.field().fill_random(1)
+    s = capi.Solver(view, maxiter=5)
+    s.start(f)
+    del ctx
+    gc.collect()
+    with pytest.raises(ValueError):
+        f.download()
+    with pytest.raises(ValueError):
+        s.iterate(1)
+    s.close()
+    f.close()
+    view.h = None  # the borrowed handle is gone with its owner
