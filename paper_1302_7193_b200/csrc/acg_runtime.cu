@@ -348,6 +348,9 @@ struct acg_context {
     // collector that finalises the context first — frees only the handle.
     mutable std::vector<acg_field*> user_fields;
     mutable std::vector<acg_solver*> user_solvers;
+    // pinned double buffer for transfers from / to pageable host memory (lazy)
+    mutable void* pin[2] = {nullptr, nullptr};
+    mutable cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     std::unique_ptr<IpcState> ipc; // peer-memory transport (acg_comm_create_ipc)
     size_t s = 8;
     bool fast() const { return math == ACG_MATH_FAST; }
@@ -512,6 +515,9 @@ void* alloc_tmp_scalars() {
 
 void destroy_cached_solver(acg_context* c);  // defined after acg_solver
 void orphan_solver(acg_solver* s);           // frees a user solver's device state, ctx = NULL
+namespace {
+void free_pinned(const acg_context* c);      // pinned transfer chunks (defined with h2d/d2h)
+}  // namespace
 
 // =================================================================== basics
 extern "C" {
@@ -708,6 +714,7 @@ acg_status acg_context_destroy(acg_context* c) {
             delete f;
         }
         for (Slab& s : c->slabs) free_slab(s);
+        free_pinned(c);
         if (c->gather) cudaFree(c->gather);
         if (c->gather_send) cudaFree(c->gather_send);
         ipc_detach(c->ipc.get());
@@ -802,6 +809,7 @@ acg_status acg_context_release_scratch(const acg_context* cc) {
             }
             free_csr(s);
         }
+        free_pinned(c);
     });
 }
 
@@ -856,6 +864,108 @@ void* staging(const acg_context* c, size_t si) {
     return s.staging;
 }
 
+// ------------------------------------------------- host <-> device transfers
+// Pinned (page-locked or registered) host buffers go straight to the DMA
+// engine. Ordinary pageable buffers (numpy arrays through the Python API)
+// move through two pinned chunks: host threads copy chunk c+1 while the DMA
+// engine moves chunk c. Measured for 1 GB (scripts/micro/h2d_paths.cu): H2D
+// 96 ms pageable -> 34 ms staged; D2H 505-526 ms -> 77-83 ms.
+constexpr size_t kPinChunk = size_t(32) << 20;
+
+bool host_is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void par_memcpy(void* dst, const void* src, size_t n) {
+    static const int nt = [] {
+        const unsigned hw = std::thread::hardware_concurrency();
+        return static_cast<int>(hw == 0 ? 1 : (hw > 8 ? 8 : hw));
+    }();
+    const size_t per = (n + nt - 1) / nt;
+    if (nt == 1 || n < (size_t(1) << 20)) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) {
+        const size_t a = t * per, b = std::min(n, a + per);
+        if (a < b)
+            th.emplace_back([=] {
+                std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+            });
+    }
+    std::memcpy(dst, src, std::min(n, per));
+    for (auto& x : th) x.join();
+}
+
+void ensure_pinned(const acg_context* c) {
+    if (c->pin[0]) return;
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaHostAlloc(&c->pin[b], kPinChunk, cudaHostAllocPortable));
+        CK(cudaEventCreateWithFlags(&c->pin_ev[b], cudaEventDisableTiming));
+        CK(cudaEventRecord(c->pin_ev[b], c->stream));
+    }
+}
+
+void free_pinned(const acg_context* c) {
+    for (int b = 0; b < 2; ++b) {
+        if (c->pin_ev[b]) cudaEventSynchronize(c->pin_ev[b]);
+        if (c->pin[b]) cudaFreeHost(c->pin[b]);
+        if (c->pin_ev[b]) cudaEventDestroy(c->pin_ev[b]);
+        c->pin[b] = nullptr;
+        c->pin_ev[b] = nullptr;
+    }
+}
+
+// Enqueue host -> device (contiguous) on the context's stream; returns once
+// `host` may be reused.
+void h2d(const acg_context* c, void* dev, const void* host, size_t n) {
+    if (n < 2 * kPinChunk || host_is_pinned(host)) {
+        CK(cudaMemcpyAsync(dev, host, n, cudaMemcpyHostToDevice, c->stream));
+        return;
+    }
+    ensure_pinned(c);
+    int k = 0;
+    for (size_t off = 0; off < n; off += kPinChunk, ++k) {
+        const size_t len = std::min(kPinChunk, n - off);
+        CK(cudaEventSynchronize(c->pin_ev[k & 1]));  // the DMA that used this chunk is done
+        par_memcpy(c->pin[k & 1], static_cast<const char*>(host) + off, len);
+        CK(cudaMemcpyAsync(static_cast<char*>(dev) + off, c->pin[k & 1], len,
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(cudaEventRecord(c->pin_ev[k & 1], c->stream));
+    }
+}
+
+// Device -> host (contiguous) after the work enqueued so far; complete on return.
+void d2h(const acg_context* c, void* host, const void* dev, size_t n) {
+    if (n < 2 * kPinChunk || host_is_pinned(host)) {
+        CK(cudaMemcpyAsync(host, dev, n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    ensure_pinned(c);
+    const size_t nch = (n + kPinChunk - 1) / kPinChunk;
+    auto issue = [&](size_t ch) {
+        const size_t off = ch * kPinChunk, len = std::min(kPinChunk, n - off);
+        CK(cudaMemcpyAsync(c->pin[ch & 1], static_cast<const char*>(dev) + off, len,
+                           cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(c->pin_ev[ch & 1], c->stream));
+    };
+    issue(0);
+    issue(1);
+    for (size_t ch = 0; ch < nch; ++ch) {
+        const size_t off = ch * kPinChunk, len = std::min(kPinChunk, n - off);
+        CK(cudaEventSynchronize(c->pin_ev[ch & 1]));
+        par_memcpy(static_cast<char*>(host) + off, c->pin[ch & 1], len);
+        if (ch + 2 < nch) issue(ch + 2);
+    }
+}
+
 template <typename T>
 void upload_t(acg_field* f, const void* host, acg_layout layout, acg_host_scope scope) {
     const acg_context* c = f->ctx;
@@ -867,20 +977,18 @@ void upload_t(acg_field* f, const void* host, acg_layout layout, acg_host_scope 
         if (layout == ACG_LAYOUT_VERTICAL) {
             const T* src = static_cast<const T*>(host) +
                            (scope == ACG_HOST_FULL ? static_cast<size_t>(s.i0) * m * n_z : 0);
-            CK(cudaMemcpyAsync(st, src, static_cast<size_t>(s.n_loc) * sizeof(T),
-                               cudaMemcpyHostToDevice, c->stream));
+            h2d(c, st, src, static_cast<size_t>(s.n_loc) * sizeof(T));
             // st[(il*m + j)*n_z + k] -> dst[il*plane + k*m + j]
             launch_transpose<T>(st, dst, n_z, m, s.m_loc, n_z, static_cast<long long>(m) * n_z, m,
                                 s.plane, c->stream);
         } else {
-            if (scope == ACG_HOST_FULL) {
+            if (scope == ACG_HOST_FULL && s.m_loc != m) {  // strided rows of this slab
                 CK(cudaMemcpy2DAsync(st, s.m_loc * sizeof(T),
                                      static_cast<const T*>(host) + s.i0, m * sizeof(T),
                                      s.m_loc * sizeof(T), static_cast<size_t>(m) * n_z,
                                      cudaMemcpyHostToDevice, c->stream));
             } else {
-                CK(cudaMemcpyAsync(st, host, static_cast<size_t>(s.n_loc) * sizeof(T),
-                                   cudaMemcpyHostToDevice, c->stream));
+                h2d(c, st, host, static_cast<size_t>(s.n_loc) * sizeof(T));
             }
             // st[(j*n_z + k)*m_loc + il] -> dst[il*plane + k*m + j]
             launch_transpose<T>(st, dst, s.m_loc, m, n_z, static_cast<long long>(n_z) * s.m_loc,
@@ -904,20 +1012,18 @@ void download_t(const acg_field* f, void* host, acg_layout layout, acg_host_scop
                                 static_cast<long long>(m) * n_z, c->stream);
             T* dst = static_cast<T*>(host) +
                      (scope == ACG_HOST_FULL ? static_cast<size_t>(s.i0) * m * n_z : 0);
-            CK(cudaMemcpyAsync(dst, st, static_cast<size_t>(s.n_loc) * sizeof(T),
-                               cudaMemcpyDeviceToHost, c->stream));
+            d2h(c, dst, st, static_cast<size_t>(s.n_loc) * sizeof(T));
         } else {
             // src[il*plane + k*m + j] -> st[(j*n_z + k)*m_loc + il]
             launch_transpose<T>(src, st, m, s.m_loc, n_z, s.plane, m,
                                 static_cast<long long>(n_z) * s.m_loc, s.m_loc, c->stream);
-            if (scope == ACG_HOST_FULL) {
+            if (scope == ACG_HOST_FULL && s.m_loc != m) {
                 CK(cudaMemcpy2DAsync(static_cast<T*>(host) + s.i0, m * sizeof(T), st,
                                      s.m_loc * sizeof(T), s.m_loc * sizeof(T),
                                      static_cast<size_t>(m) * n_z, cudaMemcpyDeviceToHost,
                                      c->stream));
             } else {
-                CK(cudaMemcpyAsync(host, st, static_cast<size_t>(s.n_loc) * sizeof(T),
-                                   cudaMemcpyDeviceToHost, c->stream));
+                d2h(c, host, st, static_cast<size_t>(s.n_loc) * sizeof(T));
             }
         }
     }
