@@ -62,3 +62,27 @@ def test_bench_scales_and_verifies(n, transport):
     assert d["n_gpus"] == n and d["value"] > 0
     v = d["verified_vs_1gpu"]
     assert v["ok"] is True and v["exact_tree"] is True
+
+
+def test_nccl_communicator_single_rank(acg):
+    """What the one-GPU pool can execute of the NCCL transport: ncclGetUniqueId,
+    ncclCommInitRank and ncclCommDestroy through acg_comm_create/destroy, and a
+    context placed on the communicator (one rank: its reduction needs no
+    exchange) solving bit-identically to the CPU reference."""
+    need(1)
+    from oracle.oracle import Oracle, Problem
+    from paper_1302_7193_b200 import capi
+    o = Oracle(Problem(32, 16))
+    comm = capi.Comm(0, 1, capi.Comm.unique_id(), 0)
+    ctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag, comm=comm)
+    f = ctx.field().fill_random(42)
+    u = ctx.field()
+    r = capi.solve(ctx, f, u_out=u, epsilon=1e-9, maxiter=200)
+    uo, ro = o.solve(o.random_field(42), epsilon=1e-9, maxiter=200)
+    assert r["iterations"] == ro.iterations
+    assert (r["residual_history"] == ro.residual_history).all()
+    assert (u.download() == uo).all()
+    for h in (f, u):
+        h.close()
+    ctx.close()
+    comm.close()
