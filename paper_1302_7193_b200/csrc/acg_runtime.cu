@@ -1788,6 +1788,7 @@ struct acg_solver {
     int cap = 0;              // device history ring capacity (entries, power of two)
     std::vector<double> hv[4];  // host copies of the histories (drained from the rings)
     int drained[4] = {0, 0, 0, 0};
+    int undrained = 0;          // step API: iterations enqueued since the last drain
     long long launches0 = 0;
     EventTimer timer;       // per-family timings (record_timings)
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
@@ -1923,6 +1924,7 @@ void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
         s->hv[a].clear();
         s->drained[a] = 0;
     }
+    s->undrained = 0;
     s->timer.st = c->stream;
     s->ktimer.st = c->stream;
     s->timer.on = s->cfg.record_timings != 0;
@@ -2223,6 +2225,26 @@ void drain_histories(acg_solver* s, const int counts[4]) {
     CK(cudaStreamSynchronize(c->stream));
 }
 
+// Step API: enqueue n iterations; every half ring of iterations the stream is
+// synchronised once and the history rings are drained (one short host stall
+// per 2048 iterations), so any number of iterate() calls keeps every entry.
+template <typename T>
+void solver_iterate_drained(acg_solver* s, int n) {
+    const int half = s->cap / 2;
+    while (n > 0) {
+        const int k = std::min(n, half - s->undrained);
+        solver_iterate<T>(s, k);
+        n -= k;
+        s->undrained += k;
+        if (s->undrained >= half) {
+            const Scalars<T> h = read_scalars<T>(s->ctx, static_cast<Scalars<T>*>(s->S[0]));
+            const int counts[4] = {h.n_res, h.n_kap, h.n_alp, h.n_bet};
+            drain_histories(s, counts);
+            s->undrained = 0;
+        }
+    }
+}
+
 // Enqueue iterations in batches; poll the done flag of the batch before the
 // current one (pipelined, so the GPU never idles on the host).
 template <typename T>
@@ -2392,7 +2414,7 @@ acg_status acg_solver_iterate(acg_solver* s, int n) {
         if (!s->ctx) fail(ACG_ERR_INVALID_ARGUMENT, "solver of a destroyed context");
         DeviceGuard g(s->ctx->device);
         CtxLock lk(s->ctx);
-        ACG_TDISPATCH(s->ctx, solver_iterate<T>(s, n));
+        ACG_TDISPATCH(s->ctx, solver_iterate_drained<T>(s, n));
     });
 }
 

@@ -137,3 +137,25 @@ def test_context_destroyed_before_its_fields(acg):
     s.close()
     f.close()
     view.h = None  # the borrowed handle is gone with its owner
+
+
+def test_step_api_histories_longer_than_the_ring(acg):
+    """The step API (acg_solver_iterate, what bench.py drives) drains the history
+    rings itself: 6000 iterations in two calls return every entry."""
+    from paper_1302_7193_b200 import capi
+    prob = Problem(96, 2, False, 10.0, 100.0)  # 5760 iterations to ||r|| < 1e-300
+    o = Oracle(prob)
+    ctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag)
+    f = ctx.field().upload(o.random_field(42))
+    s = capi.Solver(ctx, epsilon=1e-300, tau=1e-300, maxiter=6000)
+    s.start(f)
+    s.iterate(3000)
+    s.iterate(3000)
+    r = s.finish()
+    uo, ro = o.solve(o.random_field(42), epsilon=1e-300, tau=1e-300, maxiter=6000)
+    assert r["iterations"] == ro.iterations > 4096
+    for h in ("residual_history", "kappa_history", "alpha_history", "beta_history"):
+        assert np.array_equal(r[h], getattr(ro, h)), h
+    s.close()
+    f.close()
+    ctx.close()
