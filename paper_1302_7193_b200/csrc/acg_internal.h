@@ -91,6 +91,7 @@ struct Scalars {
     int n_res, n_kap, n_alp, n_bet;
     int pivot;  // written by the Thomas kernels on a zero pivot (2: stored tridiagonals)
     int hmask;  // history arrays are rings of hmask + 1 entries (the host drains them)
+    int pend;   // consumed-reduction mode: the last sweep's tree leaves await their finish
     double* h_res;
     double* h_kap;
     double* h_alp;
@@ -109,6 +110,25 @@ enum ScalarOp {
     kOpStdRnorm = 7,  // standard loop: ||r||, test                   (:236-244)
     kOpStdKappa = 8,  // standard loop: kappa, beta, it++             (:250-258)
 };
+
+// Consumed-reduction mode: instead of a reduction kernel after each sweep,
+// every CTA of the NEXT sweep reduces the previous sweep's tree leaves in its
+// prologue (the same perfect tree, so the same bits) and runs the scalar
+// program on its own copy of the state; CTA (0, 0) writes the result as the
+// other state buffer (K1 reads A and writes B, K2 reads B and writes A, so no
+// kernel reads what it writes). The last sweep's pending finish runs as one
+// tree kernel at the end of a batch of iterations.
+template <typename T>
+struct Consume {
+    const T* leaves;  // the previous sweep's tree leaves (nv arrays of nleaves)
+    int nleaves;      // power of two, <= kConsumeMaxLeaves
+    int nv;           // 1 or 2
+    int op;           // kOpIlSpmv (in K1) or kOpIlPrec (in K2)
+    const Scalars<T>* in;
+    Scalars<T>* out;
+};
+constexpr int kConsumeMaxLeaves = 1024;
+constexpr long long kConsumeK2Stage = 2LL * 131072;  // K2's leaves: third array of slab.stage
 
 // Fixed-shape pairwise reduction plan (parallel.hpp:11-20) for n values:
 // nodes at depth D are summed per thread by the reference's own rule
@@ -133,7 +153,8 @@ extern std::atomic<long long> g_launches;  // kernel launches issued (all entry 
 // written to part_* and the reduction runs k_tree1).
 template <typename T>
 int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st);
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st,
+                      const Consume<T>* cs = nullptr);
 // Once per slab: may the sweeps use the TMEM kernel with common-path
 // divisions (k_validate_tm)? Synchronous.
 template <typename T>
@@ -147,6 +168,7 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
 // 3 * max(k_tree1 blocks, kMaxFusedLeaves) values (stage 1.5 writes its nodes
 // after the leaves).
 constexpr int kMaxFusedLeaves = 131072;
+static_assert(kConsumeK2Stage == 2LL * kMaxFusedLeaves, "K2 leaves live in stage's third array");
 // Entries per device history ring (Scalars::hmask + 1); the solver loop drains
 // them to host vectors, so histories of any length fit (maxiter = 1e9 works).
 constexpr int kHistRing = 4096;
@@ -159,7 +181,14 @@ template <typename T>
 bool spmv_plane_ranges(const SlabView<T>& v, bool fast);
 template <typename T>
 int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                      const Scalars<T>* S, T* stage, cudaStream_t st);
+                      const Scalars<T>* S, T* stage, cudaStream_t st,
+                      const Consume<T>* cs = nullptr);
+// Consumed-reduction mode (small single-slab grids): applies when
+// both interleaved sweeps are the fused-reduction kernels (fp64 k_thomas_tm,
+// k_fused_spmv_pair2) and each emits at most kConsumeMaxLeaves tree leaves;
+// returns the two leaf counts.
+template <typename T>
+bool consume_plan(const SlabView<T>& v, bool phi_in_hbm, int* leaves_k1, int* leaves_k2);
 template <typename T>
 void launch_apply(const SlabView<T>& v, bool fast, const T* x, T* y, const Scalars<T>* gate,
                   cudaStream_t st);

@@ -225,7 +225,75 @@ __device__ __forceinline__ void cta_subtree_sums(const T* vals, int nv, T* __res
 }
 
 template <typename T>
-__device__ void run_op(Scalars<T>* S, int op, const T* sums);
+__device__ void run_op(Scalars<T>* S, int op, const T* sums, bool push = true);
+
+// Consumed-reduction prologue (Consume, acg_internal.h): the whole CTA reduces
+// the previous sweep's nleaves tree leaves — c consecutive leaves per thread,
+// a shuffle tree per warp, a tree over the warps: the perfect tree
+// k_tree2_wide evaluates, so the same bits — then thread 0 runs the scalar
+// program on a private copy of cs.in and CTA (0, 0) stores it to cs.out. `red`:
+// 64 values of shared memory the CTA does not use yet.
+template <typename T>
+struct Consumed {
+    T alpha, beta;
+    int done;
+};
+
+template <typename T, int NT>
+__device__ Consumed<T> consume_finish(const Consume<T>& cs, int tid, T* red) {
+    constexpr int CM = kConsumeMaxLeaves / NT;  // most leaves per thread
+    static_assert(CM >= 1 && NT % 32 == 0, "consume_finish: CTA shape");
+    __shared__ Consumed<T> res;
+    const int nl = cs.nleaves;
+    const int c = nl > NT ? nl / NT : 1;
+    const int nt = nl / c;  // threads holding leaves (power of two)
+    const int lane = tid & 31, warp = tid >> 5;
+    const int width = nt < 32 ? nt : 32;
+    for (int a = 0; a < cs.nv; ++a) {
+        T v[CM];
+        const T* lf = cs.leaves + static_cast<long long>(a) * nl + tid * c;
+#pragma unroll
+        for (int l = 0; l < CM; ++l) v[l] = (tid < nt && l < c) ? __ldcg(lf + l) : T(0);
+#pragma unroll
+        for (int w = 1; w < CM; w <<= 1)
+#pragma unroll
+            for (int l = 0; l + w < CM; l += 2 * w)
+                if (w < c) v[l] = add_rn(v[l], v[l + w]);
+        T x = v[0];
+        for (int w = 1; w < width; w <<= 1) {
+            const T o = __shfl_down_sync(0xffffffffu, x, w, width);
+            if ((lane & (2 * w - 1)) == 0) x = add_rn(x, o);
+        }
+        if (lane == 0 && tid < nt) red[a * 32 + warp] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        T sums[4] = {T(0), T(0), T(0), T(0)};
+        const int nw = (nt + 31) / 32;
+        for (int a = 0; a < cs.nv; ++a) {
+            for (int st = 1; st < nw; st <<= 1)
+                for (int w = 0; w + st < nw; w += 2 * st)
+                    red[a * 32 + w] = add_rn(red[a * 32 + w], red[a * 32 + w + st]);
+            sums[a] = red[a * 32];
+        }
+        static_assert(sizeof(Scalars<T>) % 8 == 0, "Scalars: whole 8-byte words");
+        Scalars<T> loc;
+        unsigned long long* lw = reinterpret_cast<unsigned long long*>(&loc);
+        const unsigned long long* iw = reinterpret_cast<const unsigned long long*>(cs.in);
+        for (int i = 0; i < static_cast<int>(sizeof(Scalars<T>) / 8); ++i) lw[i] = __ldcg(iw + i);
+        const bool lead = blockIdx.x == 0 && blockIdx.y == 0;
+        if (loc.pend && !loc.done) run_op(&loc, cs.op, sums, lead);
+        res.alpha = loc.alpha;
+        res.beta = loc.beta;
+        res.done = loc.done;
+        if (lead) {
+            loc.pend = loc.done ? 0 : 1;  // this sweep's leaves follow unless it is skipped
+            *cs.out = loc;
+        }
+    }
+    __syncthreads();
+    return res;
+}
 
 // ================================================================ K1 / K4
 #include "acg_thomas.cuh"
@@ -470,9 +538,17 @@ __global__ void __launch_bounds__(256)
 
 // Scalar recurrences of the PCG drivers (solver.hpp:288-364); every value
 // is computed in T and pushed to the histories as double, as in the reference.
+// One history entry: the count always advances, the store only where `push`
+// (consumed-reduction mode: every CTA runs the program, CTA (0, 0) records).
+__device__ __forceinline__ void hist(double* h, int& n, int mask, double x, bool push) {
+    if (push) h[n & mask] = x;
+    ++n;
+}
+
 template <typename T>
-__device__ void run_op(Scalars<T>* S, int op, const T* sums) {
+__device__ void run_op(Scalars<T>* S, int op, const T* sums, bool push) {
     using A = Ar<T, false>;
+    S->pend = 0;
     switch (op) {
         case kOpStore:
             for (int a = 0; a < 4; ++a) S->val[a] = sums[a];
@@ -481,7 +557,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             const T rn = sqrt_rn(sums[0]);
             S->r_norm = rn;
             S->r0 = rn;
-            S->h_res[S->n_res++ & S->hmask] = static_cast<double>(rn);
+            hist(S->h_res, S->n_res, S->hmask, static_cast<double>(rn), push);
             if (static_cast<double>(rn) <= S->tau) {
                 S->converged = 1;
                 S->done = 1;
@@ -494,7 +570,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
                 break;
             }
             S->kappa_old = sums[0];
-            S->h_kap[S->n_kap++ & S->hmask] = static_cast<double>(sums[0]);
+            hist(S->h_kap, S->n_kap, S->hmask, static_cast<double>(sums[0]), push);
             if (!(static_cast<double>(sums[0]) > 0.0)) {
                 S->error = kErrKappa;
                 S->done = 1;
@@ -512,7 +588,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             const T al = A::div(S->kappa_old, sums[0]);
             S->alpha = al;
             S->neg_alpha = -al;
-            S->h_alp[S->n_alp++ & S->hmask] = static_cast<double>(al);
+            hist(S->h_alp, S->n_alp, S->hmask, static_cast<double>(al), push);
             if (op == kOpSigma0) {
                 S->it = 1;
             } else if (op == kOpIlSpmv) {
@@ -529,7 +605,7 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             const T ka = sums[1];
             S->r_norm = rn;
             S->kappa = ka;
-            S->h_res[S->n_res++ & S->hmask] = static_cast<double>(rn);
+            hist(S->h_res, S->n_res, S->hmask, static_cast<double>(rn), push);
             S->iterations = S->it;
             if (static_cast<double>(rn) / static_cast<double>(S->r0) < S->eps ||
                 static_cast<double>(rn) < S->tau) {
@@ -537,16 +613,16 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
                 S->done = 1;
                 break;
             }
-            S->h_kap[S->n_kap++ & S->hmask] = static_cast<double>(ka);
+            hist(S->h_kap, S->n_kap, S->hmask, static_cast<double>(ka), push);
             const T be = A::div(ka, S->kappa_old);
             S->beta = be;
-            S->h_bet[S->n_bet++ & S->hmask] = static_cast<double>(be);
+            hist(S->h_bet, S->n_bet, S->hmask, static_cast<double>(be), push);
             S->kappa_old = ka;
         } break;
         case kOpStdRnorm: {
             const T rn = sqrt_rn(sums[0]);
             S->r_norm = rn;
-            S->h_res[S->n_res++ & S->hmask] = static_cast<double>(rn);
+            hist(S->h_res, S->n_res, S->hmask, static_cast<double>(rn), push);
             S->iterations = S->it;
             if (static_cast<double>(rn) / static_cast<double>(S->r0) < S->eps ||
                 static_cast<double>(rn) < S->tau) {
@@ -562,10 +638,10 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums) {
             }
             const T ka = sums[0];
             S->kappa = ka;
-            S->h_kap[S->n_kap++ & S->hmask] = static_cast<double>(ka);
+            hist(S->h_kap, S->n_kap, S->hmask, static_cast<double>(ka), push);
             const T be = A::div(ka, S->kappa_old);
             S->beta = be;
-            S->h_bet[S->n_bet++ & S->hmask] = static_cast<double>(be);
+            hist(S->h_bet, S->n_bet, S->hmask, static_cast<double>(be), push);
             S->kappa_old = ka;
             if (++S->it > S->maxiter) S->done = 1;
         } break;
@@ -996,7 +1072,8 @@ int fused_leaves(const SlabView<T>& v, int cols, const void* stage) {
 // beyond that would only wait inside tcgen05.alloc).
 template <typename T, bool Fast, bool Fused, class C>
 int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
-                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st) {
+                         Scalars<T>* S, const Scalars<T>* gate, T* stage, cudaStream_t st,
+                         const Consume<T>* cs = nullptr) {
     const unsigned tcols = thomas_tm_cols(v.n_z, sizeof(T));
     const dim3 block(32, C::W);
     constexpr int PW = C::W / C::X;  // i-planes per CTA
@@ -1024,9 +1101,27 @@ int launch_thomas_tm_cfg(const SlabView<T>& v, T* r, const T* in, T* out, T* p2,
     if (smem < floor_bytes) smem = floor_bytes;
     // fused stage 1: CTA = one aligned node (128 consecutive columns) of the tree
     const int leaves = fused_leaves(v, C::X == 4 ? C::NT : 0, Fused ? stage : nullptr);
+    if constexpr (Fused && sizeof(T) == 8) {
+        if (cs != nullptr) {
+            if (!leaves) {
+                std::fprintf(stderr, "acg: consumed reduction without fused K1 leaves\n");
+                std::abort();
+            }
+            ensure_smem(k_thomas_tm<T, Fast, Fused, C, true>, smem);
+            launch_pdl(k_thomas_tm<T, Fast, Fused, C, true>, grid, block, smem, st, v, r, in, out,
+                       p2, pk, static_cast<const Scalars<T>*>(S), gate, tcols, stage, leaves, tpc,
+                       *cs);
+            return leaves;
+        }
+    }
+    if (cs != nullptr) {
+        std::fprintf(stderr, "acg: consumed reduction requested for an fp32 sweep\n");
+        std::abort();
+    }
     ensure_smem(k_thomas_tm<T, Fast, Fused, C>, smem);
     launch_pdl(k_thomas_tm<T, Fast, Fused, C>, grid, block, smem, st, v, r, in, out, p2, pk,
-               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, tpc);
+               static_cast<const Scalars<T>*>(S), gate, tcols, leaves ? stage : nullptr, leaves, tpc,
+               Consume<T>{});
     return leaves;
 }
 
@@ -1067,8 +1162,13 @@ using ThomasTm2Default = ThomasTm2Cfg<4, 15, 15>;
 
 template <typename T, bool Fast, bool Fused>
 int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk, Scalars<T>* S,
-                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st) {
+                  const Scalars<T>* gate, T* phi_scratch, T* stage, cudaStream_t st,
+                  const Consume<T>* cs = nullptr) {
     const bool tmem = v.tm_ok && phi_scratch == nullptr;
+    if (cs != nullptr && !(tmem && sizeof(T) == 8 && thomas_tm_cols(v.n_z, sizeof(T)) <= 512)) {
+        std::fprintf(stderr, "acg: consumed reduction requested for a sweep without it\n");
+        std::abort();
+    }
     if (tmem && sizeof(T) == 4) {
         const int l = launch_thomas_tm2_cfg<T, Fast, Fused, ThomasTm2Default>(v, r, in, out, p2, pk,
                                                                              S, gate, stage, st);
@@ -1077,7 +1177,7 @@ int launch_thomas(const SlabView<T>& v, T* r, const T* in, T* out, T* p2, T* pk,
     // up to 256 columns: two CTAs per SM; 512 (fp64 n_z <= 256, fp32 <= 512): one
     if (tmem && thomas_tm_cols(v.n_z, sizeof(T)) <= 512)
         return launch_thomas_tm_cfg<T, Fast, Fused, ThomasTmDefault>(v, r, in, out, p2, pk, S, gate,
-                                                                    stage, st);
+                                                                    stage, st, cs);
     if (v.halo.on) {  // fused_halo_ok admits only the TMEM sweeps
         std::fprintf(stderr, "acg: fused halo requested for a sweep that cannot carry it\n");
         std::abort();
@@ -1125,12 +1225,13 @@ bool validate_thomas_tm(const SlabView<T>& v, cudaStream_t st) {
 
 template <typename T>
 int launch_fused_prec(const SlabView<T>& v, bool fast, T* r, T* z, const T* q, T* part_r2,
-                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st) {
+                      T* part_k, Scalars<T>* S, T* phi_scratch, T* stage, cudaStream_t st,
+                      const Consume<T>* cs) {
     const int leaves =
         fast ? launch_thomas<T, true, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
-                                            stage, st)
+                                            stage, st, cs)
              : launch_thomas<T, false, true>(v, r, q, z, part_r2, part_k, S, nullptr, phi_scratch,
-                                             stage, st);
+                                             stage, st, cs);
     post_launch("fused_prec");
     return leaves;
 }
@@ -1172,6 +1273,27 @@ bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
 }
 
 template <typename T>
+bool consume_plan(const SlabView<T>& v, bool phi_in_hbm, int* leaves_k1, int* leaves_k2) {
+    static const bool off = [] {  // ACG_CONSUME=0: reduction kernels after each sweep (A/B)
+        const char* e = std::getenv("ACG_CONSUME");
+        return e && std::string(e) == "0";
+    }();
+    if (off || sizeof(T) != 8 || v.halo.on || !v.tm_ok || phi_in_hbm || !spmv_pairs(v.m) ||
+        thomas_tm_cols(v.n_z, sizeof(T)) > 512)
+        return false;
+    // the leaf counts launch_thomas_tm_cfg and launch_fused_spmv produce (k_thomas_tm:
+    // 128-column nodes; k_fused_spmv_pair2: 512 columns, or a narrower power-of-two plane)
+    constexpr int kCols = 2 * 32 * kStencilWarps;
+    const bool narrow = v.m < kCols && v.m >= 64 && (v.m & (v.m - 1)) == 0;
+    const int a = fused_leaves(v, ThomasTmDefault::NT, v.prof);
+    const int b = fused_leaves(v, narrow ? v.m : kCols, v.prof);
+    if (a < 1 || b < 1 || a > kConsumeMaxLeaves || b > kConsumeMaxLeaves) return false;
+    *leaves_k1 = a;
+    *leaves_k2 = b;
+    return true;
+}
+
+template <typename T>
 bool spmv_plane_ranges(const SlabView<T>& v, bool fast) {
     (void)fast;
     return spmv_pairs(v.m);
@@ -1179,9 +1301,13 @@ bool spmv_plane_ranges(const SlabView<T>& v, bool fast) {
 
 template <typename T>
 int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T* z, T* part,
-                      const Scalars<T>* S, T* stage, cudaStream_t st) {
+                      const Scalars<T>* S, T* stage, cudaStream_t st, const Consume<T>* cs) {
     int leaves = 0;
     const dim3 block(32, kStencilWarps);
+    if (cs != nullptr && !(sizeof(T) == 8 && spmv_pairs(v.m) && stage != nullptr)) {
+        std::fprintf(stderr, "acg: consumed reduction requested for a sweep without it\n");
+        std::abort();
+    }
     if (v.halo.on && !(spmv_pairs(v.m) && v.plane_count == 0)) {
         std::fprintf(stderr, "acg: fused halo requested for a stencil sweep that cannot carry it\n");
         std::abort();
@@ -1236,14 +1362,28 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             constexpr int D = 3;
             const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                              static_cast<size_t>(D + 1) * 7 * kCols);
-            if (fast) {
+            if (cs != nullptr) {
+                if (!leaves) {
+                    std::fprintf(stderr, "acg: consumed reduction without fused K2 leaves\n");
+                    std::abort();
+                }
+                if (fast) {
+                    ensure_smem(k_fused_spmv_pair2<T, true, D, 2, true>, smem);
+                    launch_pdl(k_fused_spmv_pair2<T, true, D, 2, true>, g2, block, smem, st, v, u,
+                               p, q, z, part, S, stg, leaves, *cs);
+                } else {
+                    ensure_smem(k_fused_spmv_pair2<T, false, D, 2, true>, smem);
+                    launch_pdl(k_fused_spmv_pair2<T, false, D, 2, true>, g2, block, smem, st, v, u,
+                               p, q, z, part, S, stg, leaves, *cs);
+                }
+            } else if (fast) {
                 ensure_smem(k_fused_spmv_pair2<T, true, D, 2>, smem);
                 launch_pdl(k_fused_spmv_pair2<T, true, D, 2>, g2, block, smem, st, v, u, p, q, z,
-                           part, S, stg, leaves);
+                           part, S, stg, leaves, Consume<T>{});
             } else {
                 ensure_smem(k_fused_spmv_pair2<T, false, D, 2>, smem);
                 launch_pdl(k_fused_spmv_pair2<T, false, D, 2>, g2, block, smem, st, v, u, p, q, z,
-                           part, S, stg, leaves);
+                           part, S, stg, leaves, Consume<T>{});
             }
         }
     } else {
@@ -1437,13 +1577,14 @@ void launch_transpose(const T* in, T* out, int nx, int ny, int nb, long long isy
 #define ACG_INSTANTIATE(T)                                                                      \
     template bool validate_thomas_tm<T>(const SlabView<T>&, cudaStream_t);                      \
     template int launch_fused_prec<T>(const SlabView<T>&, bool, T*, T*, const T*, T*, T*,       \
-                                      Scalars<T>*, T*, T*, cudaStream_t);                       \
+                                      Scalars<T>*, T*, T*, cudaStream_t, const Consume<T>*);    \
+    template bool consume_plan<T>(const SlabView<T>&, bool, int*, int*);                        \
     template void launch_precondition<T>(const SlabView<T>&, bool, const T*, T*, Scalars<T>*,   \
                                          const Scalars<T>*, T*, cudaStream_t);                  \
     template bool spmv_plane_ranges<T>(const SlabView<T>&, bool);                               \
     template bool fused_halo_ok<T>(const SlabView<T>&, bool, bool);                              \
     template int launch_fused_spmv<T>(const SlabView<T>&, bool, T*, T*, T*, const T*, T*,       \
-                                      const Scalars<T>*, T*, cudaStream_t);                   \
+                                      const Scalars<T>*, T*, cudaStream_t, const Consume<T>*);  \
     template void launch_apply<T>(const SlabView<T>&, bool, const T*, T*, const Scalars<T>*,    \
                                   cudaStream_t);                                                \
     template void launch_residual_partials<T>(const SlabView<T>&, bool, const T*, const T*, T*, \

@@ -1793,6 +1793,11 @@ struct acg_solver {
     EventTimer timer;       // per-family timings (record_timings)
     EventTimer ktimer;      // per-launch timing of K1/K2 (bench)
     std::vector<int> leaves;  // per slab: tree leaves the last sweep wrote (fused stage 1)
+    // consumed-reduction mode (Consume, acg_internal.h): the second state buffer
+    // (K1 writes it, K2 reads it) and the K2 leaves whose finish is pending
+    void* S_alt = nullptr;
+    bool consume_pending = false;
+    int consume_leaves = 0;
     bool csr = false;         // matrix-explicit backend (standard loop on CSR + tridiagonals)
     // CUDA graph of kGraphChunk iterations (single-process contexts, small grids):
     // replayed instead of re-launching the same kernels every iteration
@@ -1812,6 +1817,8 @@ struct acg_solver {
         }
         for (void* s : S) cudaFree(s);
         S.clear();
+        if (S_alt) cudaFree(S_alt);
+        S_alt = nullptr;
         for (double* h : hist) cudaFree(h);
         hist.clear();
         if (mirror) cudaFreeHost(mirror);
@@ -1877,6 +1884,7 @@ void solver_alloc(acg_solver* s) {
             s->hist.push_back(h);
         }
     }
+    if (c->slabs.size() == 1) CK(cudaMalloc(&s->S_alt, sizeof(Scalars<T>)));
     CK(cudaHostAlloc(&s->mirror, 2 * sizeof(Scalars<T>), cudaHostAllocPortable));
     for (auto& e : s->mev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     s->u = new_field(c, false);
@@ -1986,11 +1994,72 @@ void solver_start(acg_solver* s, const acg_field* f, const acg_field* u0) {
     s->started = true;
 }
 
+// Consumed-reduction mode for this solver's loop (single slab in one process,
+// both sweeps the fused-reduction kernels with few leaves: small grids).
+template <typename T>
+bool consume_mode(const acg_solver* s, int* l1, int* l2) {
+    const acg_context* c = s->ctx;
+    if (s->S_alt == nullptr || c->slabs.size() != 1 || c->nslabs_total != 1 || c->ipc || c->comm)
+        return false;
+    return consume_plan<T>(view<T>(c, 0), c->slabs[0].phi != nullptr, l1, l2);
+}
+
+// The last K2's pending reduction finish (kOpIlSpmv on state A): one tree kernel
+// at the end of a batch, after which S[0] holds the complete state again.
+template <typename T>
+void consume_flush(acg_solver* s) {
+    if (!s->consume_pending) return;
+    const acg_context* c = s->ctx;
+    TreePlan plan{};
+    plan.blocks = s->consume_leaves;
+    launch_tree_stage2<T>(plan, static_cast<const T*>(c->slabs[0].stage) + kConsumeK2Stage, 1,
+                          static_cast<T*>(c->gather), 0, true, 1, c->exact_tree,
+                          static_cast<Scalars<T>*>(s->S[0]), kOpIlSpmv, c->stream, nullptr);
+    s->consume_pending = false;
+}
+
+// One interleaved iteration in consumed-reduction mode: K1 finishes the previous
+// K2's reduction in its prologue (state A -> B), K2 finishes K1's (B -> A).
+template <typename T>
+void iterate_interleaved_consumed(acg_solver* s, int l1, int l2) {
+    const acg_context* c = s->ctx;
+    const Slab& sl = c->slabs[0];
+    T* stage = static_cast<T*>(sl.stage);
+    Scalars<T>* A = static_cast<Scalars<T>*>(s->S[0]);
+    Scalars<T>* B = static_cast<Scalars<T>*>(s->S_alt);
+    const Consume<T> c1{stage + kConsumeK2Stage, l2, 1, kOpIlSpmv, A, B};
+    const Consume<T> c2{stage, l1, 2, kOpIlPrec, B, A};
+    const SlabView<T> v = view<T>(c, 0);
+    s->timer.begin(kFusedPrec);
+    s->ktimer.begin(kFusedPrec);
+    launch_fused_prec<T>(v, c->fast(), static_cast<T*>(s->r->data(0)),
+                         static_cast<T*>(s->z->data(0)), static_cast<const T*>(s->q->data(0)),
+                         static_cast<T*>(sl.part[0]), static_cast<T*>(sl.part[1]), A, nullptr,
+                         stage, c->stream, &c1);
+    s->ktimer.end(kFusedPrec);
+    s->timer.end(kFusedPrec);
+    s->timer.begin(kFusedSpmv);
+    s->ktimer.begin(kFusedSpmv);
+    launch_fused_spmv<T>(v, c->fast(), static_cast<T*>(s->u->data(0)),
+                         static_cast<T*>(s->p->data(0)), static_cast<T*>(s->q->data(0)),
+                         static_cast<const T*>(s->z->data(0)), static_cast<T*>(sl.part[0]), B,
+                         stage + kConsumeK2Stage, c->stream, &c2);
+    s->ktimer.end(kFusedSpmv);
+    s->timer.end(kFusedSpmv);
+    s->consume_pending = true;
+    s->consume_leaves = l2;
+}
+
 // One iteration of the interleaved loop (solver.hpp:338-365): two sweeps,
 // two reductions, all gated on the device-side `done` flag.
 template <typename T>
 void iterate_interleaved(acg_solver* s) {
     const acg_context* c = s->ctx;
+    int l1 = 0, l2 = 0;
+    if (consume_mode<T>(s, &l1, &l2)) {
+        iterate_interleaved_consumed<T>(s, l1, l2);
+        return;
+    }
     auto S = sv<T>(s);
     std::vector<int>& leaves = s->leaves;
     leaves.resize(c->slabs.size());
@@ -2119,6 +2188,7 @@ void solver_iterate_direct(acg_solver* s, int n) {
         else
             iterate_standard<T>(s);
     }
+    consume_flush<T>(s);
     CK(cudaPeekAtLastError());
 }
 

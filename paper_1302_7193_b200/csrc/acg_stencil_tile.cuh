@@ -307,11 +307,14 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     *reinterpret_cast<P*>(part + static_cast<long long>(il) * m + j) = P{siga, sigb};
 }
 
-template <typename T, bool Fast, int D, int MINB>
+// CS: consumed-reduction mode — the prologue finishes the previous K1's
+// reduction (consume_finish) instead of reading alpha, beta and done from S.
+template <typename T, bool Fast, int D, int MINB, bool CS = false>
 __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     k_fused_spmv_pair2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
-                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves) {
+                      const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves,
+                      const Consume<T> cs) {
     using A = Ar<T, Fast>;
     using P = Pair<T>;
     constexpr int NT = 32 * kStencilWarps, NS = D + 1;
@@ -322,7 +325,15 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     load_profile(prof, v.prof, 4 * n_z, tid, NT);  // static data: before the dependency wait
     __syncthreads();
     pdl_wait();  // programmatic dependent launch: the previous grid has completed
-    if (ld_dep(&S->done)) return;  // block-uniform
+    T alpha, beta;
+    if constexpr (CS) {
+        const Consumed<T> cr = consume_finish<T, NT>(cs, tid, prof + 4 * n_z);
+        if (cr.done) return;  // block-uniform
+        alpha = cr.alpha;
+        beta = cr.beta;
+    } else {
+        if (ld_dep(&S->done)) return;  // block-uniform
+    }
     int il = v.plane_begin + blockIdx.y;
     if (v.halo.on) {  // fused halo: boundary planes last, after the neighbours' K1 put them
         const int y = blockIdx.y, ml = v.m_loc;
@@ -341,7 +352,10 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     const T* dP = prof + kProfD * n_z;
     const Col<T> ca = load_col(v, il, j);
     const Col<T> cb = load_col(v, il, j + 1);
-    const T alpha = ld_dep(&S->alpha), beta = ld_dep(&S->beta);
+    if constexpr (!CS) {
+        alpha = ld_dep(&S->alpha);
+        beta = ld_dep(&S->beta);
+    }
     const long long base = static_cast<long long>(il) * v.plane + j;
     const T* zc = z + base;
     T* uc = u + base;
