@@ -1257,6 +1257,14 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
 // Measured-slower kernels (one column per thread with plain or ring loads) and
 // the other ring depths were removed after round 1.
 inline bool spmv_pairs(int m) { return m % 2 == 0; }
+// ACG_KSPLIT=0: narrow panels sweep every level in one thread (A/B)
+inline bool kseg_off() {
+    static const bool off = [] {
+        const char* e = std::getenv("ACG_KSPLIT");
+        return e && std::string(e) == "0";
+    }();
+    return off;
+}
 
 template <typename T>
 bool fused_halo_ok(const SlabView<T>& v, bool fast, bool phi_in_hbm) {
@@ -1362,29 +1370,41 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             constexpr int D = 3;
             const size_t smem = sizeof(T) * (4 * static_cast<size_t>(v.n_z) +
                                              static_cast<size_t>(D + 1) * 7 * kCols);
-            if (cs != nullptr) {
-                if (!leaves) {
-                    std::fprintf(stderr, "acg: consumed reduction without fused K2 leaves\n");
-                    std::abort();
-                }
-                if (fast) {
-                    ensure_smem(k_fused_spmv_pair2<T, true, D, 2, true>, smem);
-                    launch_pdl(k_fused_spmv_pair2<T, true, D, 2, true>, g2, block, smem, st, v, u,
-                               p, q, z, part, S, stg, leaves, *cs);
-                } else {
-                    ensure_smem(k_fused_spmv_pair2<T, false, D, 2, true>, smem);
-                    launch_pdl(k_fused_spmv_pair2<T, false, D, 2, true>, g2, block, smem, st, v, u,
-                               p, q, z, part, S, stg, leaves, *cs);
-                }
-            } else if (fast) {
-                ensure_smem(k_fused_spmv_pair2<T, true, D, 2>, smem);
-                launch_pdl(k_fused_spmv_pair2<T, true, D, 2>, g2, block, smem, st, v, u, p, q, z,
-                           part, S, stg, leaves, Consume<T>{});
-            } else {
-                ensure_smem(k_fused_spmv_pair2<T, false, D, 2>, smem);
-                launch_pdl(k_fused_spmv_pair2<T, false, D, 2>, g2, block, smem, st, v, u, p, q, z,
-                           part, S, stg, leaves, Consume<T>{});
+            // narrow panels with the fused reduction: 512/m level groups per plane
+            // (KS), their products of levels past group 0's in shared memory
+            int kseg = narrow && stg != nullptr ? kCols / v.m : 1;
+            size_t smem_ks = smem;
+            if (kseg > 1) {
+                const int len = (v.n_z + kseg - 1) / kseg;
+                smem_ks += sizeof(T) * static_cast<size_t>(v.n_z - len) * v.m;
+                if (smem_ks > 232448 || kseg_off()) kseg = 1;
             }
+            const Consume<T> none{};
+            const Consume<T>& c2 = cs ? *cs : none;
+            if (cs != nullptr && !leaves) {
+                std::fprintf(stderr, "acg: consumed reduction without fused K2 leaves\n");
+                std::abort();
+            }
+#define ACG_PAIR2(FAST, CSM, KSM)                                                               \
+    do {                                                                                        \
+        auto kern = k_fused_spmv_pair2<T, FAST, D, 2, CSM, KSM>;                                \
+        const size_t sb = KSM ? smem_ks : smem;                                                 \
+        ensure_smem(kern, sb);                                                                  \
+        launch_pdl(kern, g2, block, sb, st, v, u, p, q, z, part, S, stg, leaves, c2, kseg);     \
+    } while (0)
+            const bool ks = kseg > 1, csm = cs != nullptr;
+            if (fast) {
+                if (csm && ks) ACG_PAIR2(true, true, true);
+                else if (csm) ACG_PAIR2(true, true, false);
+                else if (ks) ACG_PAIR2(true, false, true);
+                else ACG_PAIR2(true, false, false);
+            } else {
+                if (csm && ks) ACG_PAIR2(false, true, true);
+                else if (csm) ACG_PAIR2(false, true, false);
+                else if (ks) ACG_PAIR2(false, false, true);
+                else ACG_PAIR2(false, false, false);
+            }
+#undef ACG_PAIR2
         }
     } else {
         constexpr int D = 5;  // shared z-tile ring depth

@@ -309,12 +309,20 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
 
 // CS: consumed-reduction mode — the prologue finishes the previous K1's
 // reduction (consume_finish) instead of reading alpha, beta and done from S.
-template <typename T, bool Fast, int D, int MINB, bool CS = false>
+// KS: level split for narrow panels (CTA = one plane of m < 512 columns, so only
+// m/2 of the 256 threads would hold a column pair): kseg = 512/m groups of m/2
+// threads sweep consecutive level ranges of the same columns — every level's
+// u, p, q are independent of the others, only the vertical neighbours z(k-1),
+// z(k+1) cross a range boundary and are plain loads. <p, q> stays the
+// reference's sequential sum over k (operator.hpp:395-404): group 0 sums its
+// levels on the fly, groups >= 1 park their products in shared memory, and
+// group 0 continues the same running sum through them in level order.
+template <typename T, bool Fast, int D, int MINB, bool CS = false, bool KS = false>
 __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     k_fused_spmv_pair2(const SlabView<T> v, T* __restrict__ u, T* __restrict__ p,
                       T* __restrict__ q, const T* __restrict__ z, T* __restrict__ part,
                       const Scalars<T>* __restrict__ S, T* __restrict__ stage, int nleaves,
-                      const Consume<T> cs) {
+                      const Consume<T> cs, int kseg) {
     using A = Ar<T, Fast>;
     using P = Pair<T>;
     constexpr int NT = 32 * kStencilWarps, NS = D + 1;
@@ -341,11 +349,22 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         if (il == 0 && v.halo.ghost[0] != nullptr) halo_acquire(v.halo.wait_flag[0], v.halo.seq);
         if (il == ml - 1 && v.halo.ghost[1] != nullptr) halo_acquire(v.halo.wait_flag[1], v.halo.seq);
     }
-    const int jr = blockIdx.x * 2 * NT + 2 * tid;
+    int jr = blockIdx.x * 2 * NT + 2 * tid;
+    int grp = 0, k0 = 0, k1 = n_z;  // KS: this thread's level group and range
+    if constexpr (KS) {
+        const int half = m >> 1;  // column pairs per plane; kseg * half == NT
+        grp = tid / half;
+        jr = 2 * (tid - grp * half);
+        const int len = (n_z + kseg - 1) / kseg;
+        k0 = min(n_z, grp * len);
+        k1 = min(n_z, k0 + len);
+    }
     const bool valid = jr < m;  // m even: both columns exist
     if (stage == nullptr && !valid) return;
     const int j = valid ? jr : m - 2;
     P* ring = reinterpret_cast<P*>(prof + 4 * n_z) + tid;  // [slot][7][NT] (6 pairs + 2 edge scalars)
+    // KS: products of levels [len, n_z) as pairs [k - len][m / 2], after the ring
+    P* prod = reinterpret_cast<P*>(prof + 4 * n_z) + NS * 7 * NT;
     const T* sP = prof + kProfS * n_z;
     const T* bP = prof + kProfB * n_z;
     const T* cP = prof + kProfC * n_z;
@@ -384,12 +403,17 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         };
     #pragma unroll
         for (int t = 0; t < D; ++t) {
-            if (t < n_z) issue(t, t);
+            if (k0 + t < k1) issue(k0 + t, t);
             cp_commit();
         }
-        P z0 = *reinterpret_cast<const P*>(zc), zd = z0;
+        P z0{T(0), T(0)}, zd{T(0), T(0)};
+        if (k0 < k1) {
+            z0 = *reinterpret_cast<const P*>(zc + static_cast<long long>(k0) * sm);
+            zd = k0 > 0 ? *reinterpret_cast<const P*>(zc + static_cast<long long>(k0 - 1) * sm) : z0;
+        }
+        const int len = KS ? (n_z + kseg - 1) / kseg : 0;  // KS: group 0's level count
         int cs = 0, ps_ = D;
-        for (int k = 0; k < n_z; ++k) {
+        for (int k = k0; k < k1; ++k) {
             const long long l = static_cast<long long>(k) * sm;
             cp_wait<D - 1>();
             const P* r0 = ring + cs * 7 * NT;
@@ -399,7 +423,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
             const P ce = r0[4 * NT], cw = r0[5 * NT];
             const P ex = r0[6 * NT];
             const T cs0 = ex.x, cn1 = ex.y;
-            if (k + D < n_z) issue(k + D, ps_);
+            if (k + D < k1) issue(k + D, ps_);
             cp_commit();
             cs = cs + 1 == NS ? 0 : cs + 1;
             ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
@@ -416,8 +440,12 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
                                            cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
             qv.x = A::add(qv.x, A::mul(dP[k], dqa));
             qv.y = A::add(qv.y, A::mul(dP[k], dqb));
-            siga = A::add(siga, A::mul(pv.x, qv.x));
-            sigb = A::add(sigb, A::mul(pv.y, qv.y));
+            if (KS && grp > 0) {
+                prod[(k - len) * (m >> 1) + (j >> 1)] = P{A::mul(pv.x, qv.x), A::mul(pv.y, qv.y)};
+            } else {
+                siga = A::add(siga, A::mul(pv.x, qv.x));
+                sigb = A::add(sigb, A::mul(pv.y, qv.y));
+            }
             if (valid) {
                 st_pair_cs(uc + l, un);
                 st_pair_cs(pc + l, pv);
@@ -427,6 +455,19 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
             z0 = zu;
         }
         cp_wait<0>();
+    }
+    if constexpr (KS) {  // group 0 carries the running sums through the later levels
+        __syncthreads();
+        if (grp == 0) {
+            const int len = (n_z + kseg - 1) / kseg;
+            for (int k = len; k < n_z; ++k) {
+                const P pq = prod[(k - len) * (m >> 1) + (j >> 1)];
+                siga = A::add(siga, pq.x);
+                sigb = A::add(sigb, pq.y);
+            }
+        } else {
+            siga = sigb = T(0);
+        }
     }
     if (stage != nullptr) {  // fused reduction stage 1: the CTA's 512 columns are a tree node
         __syncthreads();
