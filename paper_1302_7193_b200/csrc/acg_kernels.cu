@@ -230,9 +230,10 @@ __device__ void run_op(Scalars<T>* S, int op, const T* sums, bool push = true);
 // Consumed-reduction prologue (Consume, acg_internal.h): the whole CTA reduces
 // the previous sweep's nleaves tree leaves — c consecutive leaves per thread,
 // a shuffle tree per warp, a tree over the warps: the perfect tree
-// k_tree2_wide evaluates, so the same bits — then thread 0 runs the scalar
-// program on a private copy of cs.in and CTA (0, 0) stores it to cs.out. `red`:
-// 64 values of shared memory the CTA does not use yet.
+// k_tree2_wide evaluates, so the same bits — while its last warp fetches the
+// state cs.in into shared memory, one word per thread; thread 0 runs the
+// scalar program there and CTA (0, 0) stores the result to cs.out. `red`: 64
+// values of shared memory the CTA does not use yet.
 template <typename T>
 struct Consumed {
     T alpha, beta;
@@ -242,8 +243,15 @@ struct Consumed {
 template <typename T, int NT>
 __device__ Consumed<T> consume_finish(const Consume<T>& cs, int tid, T* red) {
     constexpr int CM = kConsumeMaxLeaves / NT;  // most leaves per thread
-    static_assert(CM >= 1 && NT % 32 == 0, "consume_finish: CTA shape");
+    constexpr int NW = static_cast<int>(sizeof(Scalars<T>) / 8);
+    static_assert(CM >= 1 && NT % 32 == 0 && NW <= 32, "consume_finish: CTA shape");
+    static_assert(sizeof(Scalars<T>) % 8 == 0, "Scalars: whole 8-byte words");
     __shared__ Consumed<T> res;
+    __shared__ __align__(8) unsigned long long state[NW];
+    // the last warp also fetches the state words, one each, while the leaves load
+    if (tid >= NT - 32 && tid - (NT - 32) < NW)
+        state[tid - (NT - 32)] =
+            __ldcg(reinterpret_cast<const unsigned long long*>(cs.in) + (tid - (NT - 32)));
     const int nl = cs.nleaves;
     const int c = nl > NT ? nl / NT : 1;
     const int nt = nl / c;  // threads holding leaves (power of two)
@@ -276,22 +284,17 @@ __device__ Consumed<T> consume_finish(const Consume<T>& cs, int tid, T* red) {
                     red[a * 32 + w] = add_rn(red[a * 32 + w], red[a * 32 + w + st]);
             sums[a] = red[a * 32];
         }
-        static_assert(sizeof(Scalars<T>) % 8 == 0, "Scalars: whole 8-byte words");
-        Scalars<T> loc;
-        unsigned long long* lw = reinterpret_cast<unsigned long long*>(&loc);
-        const unsigned long long* iw = reinterpret_cast<const unsigned long long*>(cs.in);
-        for (int i = 0; i < static_cast<int>(sizeof(Scalars<T>) / 8); ++i) lw[i] = __ldcg(iw + i);
+        Scalars<T>* loc = reinterpret_cast<Scalars<T>*>(state);  // the program runs in shared memory
         const bool lead = blockIdx.x == 0 && blockIdx.y == 0;
-        if (loc.pend && !loc.done) run_op(&loc, cs.op, sums, lead);
-        res.alpha = loc.alpha;
-        res.beta = loc.beta;
-        res.done = loc.done;
-        if (lead) {
-            loc.pend = loc.done ? 0 : 1;  // this sweep's leaves follow unless it is skipped
-            *cs.out = loc;
-        }
+        if (loc->pend && !loc->done) run_op(loc, cs.op, sums, lead);
+        res.alpha = loc->alpha;
+        res.beta = loc->beta;
+        res.done = loc->done;
+        loc->pend = loc->done ? 0 : 1;  // this sweep's leaves follow unless it is skipped
     }
     __syncthreads();
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid < NW)  // CTA (0, 0): the next state
+        reinterpret_cast<unsigned long long*>(cs.out)[tid] = state[tid];
     return res;
 }
 
@@ -1373,6 +1376,7 @@ int launch_fused_spmv(const SlabView<T>& v, bool fast, T* u, T* p, T* q, const T
             // narrow panels with the fused reduction: 512/m level groups per plane
             // (KS), their products of levels past group 0's in shared memory
             int kseg = narrow && stg != nullptr ? kCols / v.m : 1;
+            // (ring depth 3 as for wide panels; depth 5, one CTA per SM: C1 K2 slower)
             size_t smem_ks = smem;
             if (kseg > 1) {
                 const int len = (v.n_z + kseg - 1) / kseg;
