@@ -7,8 +7,10 @@ even m) / k_fused_spmv_quad (fp32, m % 4 == 0) / k_fused_spmv_pair (fp32, other
 even m), k_fused_spmv_tile for odd m; reduction
 stage 2 = k_tree2_wide / k_tree2_shfl / k_tree2 by leaf count. The worker
 (tests/variant_worker.py) runs shapes that reach each of them, in one process
-per launch-mode setting: the default and programmatic dependent launch off
-(ACG_PDL=0).
+per launch-mode setting: the default, programmatic dependent launch off
+(ACG_PDL=0), a reduction kernel after every sweep instead of the consumed
+reductions of small single-slab grids (ACG_CONSUME=0), and narrow-panel K2
+without the level split (ACG_KSPLIT=0).
 """
 import os
 import subprocess
@@ -22,6 +24,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 VARIANTS = {
     "default": {},
     "no_pdl": {"ACG_PDL": "0"},
+    "no_consume": {"ACG_CONSUME": "0"},
+    "no_ksplit": {"ACG_KSPLIT": "0"},
 }
 
 

@@ -1,7 +1,7 @@
 """Worker for tests/test_variants.py: one process per kernel-variant setting.
 
-The launch-mode switch ACG_PDL is read once per process,
-so each setting runs in its own process. It runs the fused sweeps, apply,
+The launch-mode switches (ACG_PDL, ACG_CONSUME, ACG_KSPLIT) are read once per
+process, so each setting runs in its own process. It runs the fused sweeps, apply,
 precondition and two full solves (fp64 and fp32, over SHAPES) and compares them bit for bit with the CPU oracle.
 Prints VARIANT_OK or the first mismatch.
 """
@@ -51,6 +51,26 @@ def check(m, n_z, dtype):
             return h
     if not np.array_equal(ug, uo):
         return "solution"
+    # the step API in uneven batches (graph chunks, direct remainders, the
+    # consumed-reduction flush at every batch end) against one oracle solve
+    from paper_1302_7193_b200 import capi
+    cc = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag,
+                      dtype=capi.F32 if dtype == np.float32 else capi.F64)
+    fd = cc.field().upload(f)
+    sv = capi.Solver(cc, epsilon=1e-300, tau=1e-300, maxiter=41)
+    sv.start(fd)
+    for n in (5, 17, 3, 16):
+        sv.iterate(n)
+    rs = sv.finish()
+    _, ro = o.solve(f, epsilon=1e-300, tau=1e-300, maxiter=41)
+    ok = rs["iterations"] == ro.iterations and all(
+        np.array_equal(rs[h], getattr(ro, h))
+        for h in ("residual_history", "kappa_history", "alpha_history", "beta_history"))
+    sv.close()
+    fd.close()
+    cc.close()
+    if not ok:
+        return "step API batches"
     return None
 
 
@@ -59,7 +79,10 @@ def check(m, n_z, dtype):
 # columns whose z' needs all 512 TMEM columns (one CTA per SM: n_z 160), and
 # columns taller than TMEM holds (k_thomas, z' in global memory: fp64 n_z 272,
 # fp32 n_z 520)
-SHAPES = ((128, 24), (66, 19), (65, 12), (32, 160), (16, 272), (8, 520))
+# and power-of-two panels m < 512 whose K2 splits the levels over 512/m thread
+# groups in one CTA (fp64: 8, 4, 2 groups, ragged last group) with the
+# consumed-reduction prologues
+SHAPES = ((128, 24), (66, 19), (65, 12), (32, 160), (16, 272), (8, 520), (64, 13), (256, 33))
 
 
 def main():
