@@ -333,13 +333,8 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     load_profile(prof, v.prof, 4 * n_z, tid, NT);  // static data: before the dependency wait
     __syncthreads();
     pdl_wait();  // programmatic dependent launch: the previous grid has completed
-    T alpha, beta;
-    if constexpr (CS) {
-        const Consumed<T> cr = consume_finish<T, NT>(cs, tid, prof + 4 * n_z);
-        if (cr.done) return;  // block-uniform
-        alpha = cr.alpha;
-        beta = cr.beta;
-    } else {
+    T alpha = T(0), beta = T(0);
+    if constexpr (!CS) {
         if (ld_dep(&S->done)) return;  // block-uniform
     }
     int il = v.plane_begin + blockIdx.y;
@@ -382,12 +377,12 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
     T* qc = q + base;
     const long long sm = m;
     T siga = T(0), sigb = T(0);
-    if (valid) {  // the idle warps of a narrow panel's CTA (fused reduction) skip the sweep
-        long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
-        if (v.halo.on) {  // ghost rows straight from this rank's mailbox
-            if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
-            if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
-        }
+    long long oe = ca.oe, ow = ca.ow;  // same for both columns (same plane)
+    if (v.halo.on) {  // ghost rows straight from this rank's mailbox
+        if (il == 0 && v.halo.ghost[0] != nullptr) ow = (v.halo.ghost[0] + j) - zc;
+        if (il == v.m_loc - 1 && v.halo.ghost[1] != nullptr) oe = (v.halo.ghost[1] + j) - zc;
+    }
+    {
         auto issue = [&](int k, int s) {
             const long long l = static_cast<long long>(k) * sm;
             P* r0 = ring + s * 7 * NT;
@@ -401,11 +396,23 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
             cpa(e, zc + l + ca.os);
             cpa(e + 1, zc + l + 1 + cb.on);
         };
+        // the idle warps of a narrow panel's CTA (fused reduction) skip the sweep
     #pragma unroll
         for (int t = 0; t < D; ++t) {
-            if (k0 + t < k1) issue(k0 + t, t);
+            if (valid && k0 + t < k1) issue(k0 + t, t);
             cp_commit();
         }
+        if constexpr (CS) {  // the previous reduction's finish while the ring fills
+            __shared__ T cs_red[64];
+            const Consumed<T> cr = consume_finish<T, NT>(cs, tid, cs_red);
+            if (cr.done) {  // block-uniform
+                cp_wait<0>();
+                return;
+            }
+            alpha = cr.alpha;
+            beta = cr.beta;
+        }
+        if (!valid) goto swept;
         P z0{T(0), T(0)}, zd{T(0), T(0)};
         if (k0 < k1) {
             z0 = *reinterpret_cast<const P*>(zc + static_cast<long long>(k0) * sm);
@@ -456,6 +463,7 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
         }
         cp_wait<0>();
     }
+swept:
     if constexpr (KS) {  // group 0 carries the running sums through the later levels
         __syncthreads();
         if (grp == 0) {
