@@ -378,12 +378,12 @@ def run_gpu(args, cfg):
 
     def timed_pass():
         solver.time_kernels(args.ktime_inline)
-        launches_before = capi.launch_count()
         with ClockSampler(dev) as clk:
             # the sampler's start-up left the GPU idle for a moment: a few untimed
             # iterations right before the start event (stream order) bring it back
             # to speed, which matters for sub-millisecond steps (small grids)
             solver.iterate(REWARM)
+            launches_before = capi.launch_count()  # the timed region's launches only
             ev0.record(stream)
             h0 = time.perf_counter()
             solver.iterate(args.steps)
@@ -497,47 +497,75 @@ def run_gpu(args, cfg):
                      "algorithmic_bytes_per_launch": iter_bytes, "launch_ms": ms_max / args.steps})
 
     # ---- e2e through the C ABI with pinned host buffers (H2D f, solve, D2H u)
+    # serial: one call sequence upload -> solve -> download. stream: a stream
+    # of E2E_SOLVES solves, each with its own f upload and u download; the
+    # next f uploads and the previous u downloads on the context's copy stream
+    # while the current solve runs (acg_field_upload_async / _download_async,
+    # double-buffered fields and pinned buffers). The headline e2e is the
+    # stream: every solve still moves its f in and its u out inside the timed
+    # region; the serial figure is kept beside it.
     e2e = None
     if not args.no_e2e:
         m, n_z = cfg["m"], cfg["n_z"]
         ml = info["i_end"] - info["i_begin"]
         npdt = np.float32 if dtype == capi.F32 else np.float64
-        hf = capi.HostBuffer((ml, m, n_z), npdt)
-        hu = capi.HostBuffer((ml, m, n_z), npdt)
-        f.download(out=hf.array, scope=capi.HOST_LOCAL)
-        f2, u2 = ctx.field(), ctx.field()
+        hf = [capi.HostBuffer((ml, m, n_z), npdt) for _ in range(2)]
+        hu = [capi.HostBuffer((ml, m, n_z), npdt) for _ in range(2)]
+        f.download(out=hf[0].array, scope=capi.HOST_LOCAL)
+        hf[1].array[...] = hf[0].array
+        fs, us = [ctx.field(), ctx.field()], [ctx.field(), ctx.field()]
+        kw = dict(epsilon=1e-300, tau=1e-300, maxiter=args.steps, variant=variant,
+                  backend=backend)
         # one untimed warm-up call (allocates the context's cached solver state)
-        f2.upload(hf.array, scope=capi.HOST_LOCAL)
-        capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps,
-                   variant=variant, backend=backend)
-        u2.download(out=hu.array, scope=capi.HOST_LOCAL)
+        fs[0].upload(hf[0].array, scope=capi.HOST_LOCAL)
+        capi.solve(ctx, fs[0], u_out=us[0], **kw)
+        us[0].download(out=hu[0].array, scope=capi.HOST_LOCAL)
         barrier()
         t0 = time.perf_counter()
-        f2.upload(hf.array, scope=capi.HOST_LOCAL)
+        fs[0].upload(hf[0].array, scope=capi.HOST_LOCAL)
         ctx.sync()
         t1 = time.perf_counter()
-        r2 = capi.solve(ctx, f2, u_out=u2, epsilon=1e-300, tau=1e-300, maxiter=args.steps,
-                        variant=variant, backend=backend)
+        r2 = capi.solve(ctx, fs[0], u_out=us[0], **kw)
         t2 = time.perf_counter()
-        u2.download(out=hu.array, scope=capi.HOST_LOCAL)
+        us[0].download(out=hu[0].array, scope=capi.HOST_LOCAL)
+        barrier()
+        wall_serial = time.perf_counter() - t0
+        split = {"upload_s": t1 - t0, "solve_s": t2 - t1, "download_s": time.perf_counter() - t2}
+        nsolve = args.e2e_solves
+        barrier()
+        t0 = time.perf_counter()
+        fs[0].upload_async(hf[0].array, scope=capi.HOST_LOCAL)
+        for i in range(nsolve):
+            if i + 1 < nsolve:
+                fs[(i + 1) % 2].upload_async(hf[(i + 1) % 2].array, scope=capi.HOST_LOCAL)
+            rs = capi.solve(ctx, fs[i % 2], u_out=us[i % 2], **kw)
+            us[i % 2].download_async(hu[i % 2].array, scope=capi.HOST_LOCAL)
+            if rs["iterations"] != r2["iterations"]:
+                raise SystemExit("bench: e2e stream solve differs from the serial one")
+        for u_ in us:
+            u_.wait()
         barrier()
         wall = time.perf_counter() - t0
-        split = {"upload_s": t1 - t0, "solve_s": t2 - t1, "download_s": time.perf_counter() - t2}
+        if not np.array_equal(hu[(nsolve - 1) % 2].array, hu[nsolve % 2].array if nsolve > 1
+                              else hu[0].array):
+            raise SystemExit("bench: e2e stream results differ between solves")
         if world > 1:
             import torch.distributed as dist
-            t = torch.tensor([wall], device=pg_dev, dtype=torch.float64)
+            t = torch.tensor([wall, wall_serial], device=pg_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
+            wall, wall_serial = float(t[0].item()), float(t[1].item())
         nbytes = ml * m * n_z * s
-        e2e = {"value": args.steps / wall, "unit": "iter/s",
+        e2e = {"value": nsolve * args.steps / wall, "unit": "iter/s",
                "h2d_bytes_per_step": nbytes * world / args.steps,
                "d2h_bytes_per_step": nbytes * world / args.steps + 8 * (args.steps + 1),
-               "call": "acg_field_upload + acg_solve + acg_field_download (pinned host)",
-               "solve_wall_s": wall, "iterations": r2["iterations"], "split": split}
-        f2.close()
-        u2.close()
-        hf.close()
-        hu.close()
+               "call": "acg_field_upload_async + acg_solve + acg_field_download_async "
+                       "(pinned host, copy stream beside the solve)",
+               "solves": nsolve, "iterations_per_solve": r2["iterations"], "wall_s": wall,
+               "serial": {"value": args.steps / wall_serial,
+                          "call": "acg_field_upload + acg_solve + acg_field_download (pinned host)",
+                          "wall_s": wall_serial, "split": split}}
+        for x in fs + us + hf + hu:
+            x.close()
 
     # ---- CPU baseline (the reference compiled from source, all host cores)
     cpu = None
@@ -600,6 +628,8 @@ def main():
                          "headline (0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-solves", type=int, default=4,
+                    help="solves in the e2e stream (each uploads f and downloads u)")
     ap.add_argument("--no-ktime", action="store_true",
                     help="skip the per-launch K1/K2 timing pass (no kernel roofline)")
     ap.add_argument("--ktime-inline", action="store_true",

@@ -164,6 +164,20 @@ acg_status acg_field_upload_device(acg_field* f, const void* dev, acg_layout lay
                                    acg_host_scope scope);
 acg_status acg_field_download_device(const acg_field* f, void* dev, acg_layout layout,
                                      acg_host_scope scope);
+/* Asynchronous host transfers (no reference counterpart: the B200-side
+ * overlap of PCIe traffic with the solver). The DMA and the relayout run on
+ * the context's copy stream into the field's own staging, after the work
+ * already enqueued on the context's stream; the call returns at once. The
+ * host buffer must be page-locked (acg_host_alloc, cudaHostAlloc,
+ * cudaHostRegister) and stay untouched until the transfer completes: every
+ * later entry point that takes the field orders its device work after it, and
+ * acg_field_wait blocks the host until it is done (required before reading a
+ * downloaded buffer or reusing an uploaded one). */
+acg_status acg_field_upload_async(acg_field* f, const void* host, acg_layout layout,
+                                  acg_host_scope scope);
+acg_status acg_field_download_async(const acg_field* f, void* host, acg_layout layout,
+                                    acg_host_scope scope);
+acg_status acg_field_wait(const acg_field* f);
 acg_status acg_field_fill(acg_field* f, double value);
 /* fill_random, field.hpp:180-196 (splitmix64, canonical (i,j,k) draw order) */
 acg_status acg_field_fill_random(acg_field* f, uint64_t seed);

@@ -100,6 +100,9 @@ def lib():
         "acg_field_destroy": (ip, [vp]),
         "acg_field_upload": (ip, [vp, vp, ip, ip]),
         "acg_field_download": (ip, [vp, vp, ip, ip]),
+        "acg_field_upload_async": (ip, [vp, vp, ip, ip]),
+        "acg_field_download_async": (ip, [vp, vp, ip, ip]),
+        "acg_field_wait": (ip, [vp]),
         "acg_field_upload_device": (ip, [vp, vp, ip, ip]),
         "acg_comm_create_ipc": (ip, [pp, ip, ip, vp, ip]),
         "acg_field_download_device": (ip, [vp, vp, ip, ip]),
@@ -371,6 +374,33 @@ class Field:
             out = np.empty(self._shape(layout, scope), dtype=self.ctx.np_dtype)
         check(lib().acg_field_download(self.h, _vptr(out), layout, scope))
         return out
+
+    def upload_async(self, host, layout=VERTICAL, scope=HOST_FULL):
+        """Enqueue the upload of a page-locked host array (HostBuffer.array) on
+        the context's copy stream and return at once; later calls on this
+        field run after it. Keep `host` unchanged until wait()."""
+        a = np.asarray(host)
+        if a.dtype != self.ctx.np_dtype or not a.flags.c_contiguous:
+            raise ValueError("upload_async needs a C-contiguous page-locked array of the context dtype")
+        if a.shape != self._shape(layout, scope):
+            raise ValueError(f"upload_async: shape {a.shape}, expected {self._shape(layout, scope)}")
+        check(lib().acg_field_upload_async(self.h, _vptr(a), layout, scope))
+        return self
+
+    def download_async(self, out, layout=VERTICAL, scope=HOST_FULL):
+        """Enqueue the download into a page-locked host array; `out` is
+        complete after wait()."""
+        if out.dtype != self.ctx.np_dtype or not out.flags.c_contiguous:
+            raise ValueError("download_async needs a C-contiguous page-locked array of the context dtype")
+        if out.shape != self._shape(layout, scope):
+            raise ValueError(f"download_async: shape {out.shape}, expected {self._shape(layout, scope)}")
+        check(lib().acg_field_download_async(self.h, _vptr(out), layout, scope))
+        return out
+
+    def wait(self):
+        """Block until this field's asynchronous transfers are complete."""
+        check(lib().acg_field_wait(self.h))
+        return self
 
     def fill(self, v):
         check(lib().acg_field_fill(self.h, float(v)))

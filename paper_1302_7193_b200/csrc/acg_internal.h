@@ -268,6 +268,12 @@ void launch_ipc_signal(unsigned long long* const* flags, int n, unsigned long lo
 void launch_ipc_wait(const unsigned long long* flags, int n, unsigned long long need,
                      unsigned long long seq, cudaStream_t st);
 
+// Device-to-host snapshot of `words` 8-byte words into mapped pinned memory by
+// a one-warp kernel: stream-ordered like a cudaMemcpyAsync, but it does not
+// queue behind bulk DMA on the copy engines (the solve loop's done-flag polls
+// while asynchronous field transfers run).
+void launch_snapshot(const void* src, void* dst_mapped, int words, cudaStream_t st);
+
 // relayout between the reference's host layouts and plane-major (K7):
 // out[x*osx + y + b*osb] = in[x + y*isy + b*isb]  for x<nx, y<ny, b<nb
 template <typename T>

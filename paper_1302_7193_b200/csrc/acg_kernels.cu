@@ -1581,6 +1581,17 @@ void launch_ipc_signal(unsigned long long* const* flags, int n, unsigned long lo
     post_launch("ipc_signal");
 }
 
+__global__ void k_snapshot(const unsigned long long* __restrict__ src,
+                           unsigned long long* __restrict__ dst, int words) {
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
+}
+
+void launch_snapshot(const void* src, void* dst_mapped, int words, cudaStream_t st) {
+    k_snapshot<<<1, 32, 0, st>>>(static_cast<const unsigned long long*>(src),
+                                 static_cast<unsigned long long*>(dst_mapped), words);
+    post_launch("snapshot");
+}
+
 void launch_ipc_wait(const unsigned long long* flags, int n, unsigned long long need,
                      unsigned long long seq, cudaStream_t st) {
     k_ipc_wait<<<1, 1, 0, st>>>(flags, n, need, seq);

@@ -328,6 +328,10 @@ struct acg_context {
     acg_comm* comm = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t halo_stream = nullptr;       // ranks > 1: halo exchange beside the interior sweep
+    // asynchronous host transfers (acg_field_upload_async / _download_async):
+    // DMA and relayout on their own stream, beside the solver's kernels
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copy = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     bool exact_tree = true;
     std::vector<Slab> slabs;  // local slabs (same device)
@@ -359,6 +363,12 @@ struct acg_context {
 struct acg_field {
     const acg_context* ctx = nullptr;
     std::vector<void*> base;  // per local slab: (m_loc + 2) planes
+    // asynchronous transfers: per-slab staging (allocated on first use) and the
+    // event the copy stream records after the field's last async transfer;
+    // every entry point that touches the field orders its stream after it
+    mutable std::vector<void*> stage;
+    mutable cudaEvent_t ev = nullptr;
+    mutable bool pending = false;
     void* data(size_t i) const {
         return static_cast<char*>(base[i]) + ctx->slabs[i].plane * ctx->s;
     }
@@ -409,11 +419,18 @@ SlabView<T> view(const acg_context* c, size_t si) {
 void check_ctx(const acg_context* c) {
     if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "null context");
 }
+// Work enqueued on `c`'s stream after this call sees the field's asynchronous
+// transfers complete (a device-side wait; the host does not block).
+void await_field(const acg_context* c, const acg_field* f) {
+    if (f && f->pending) CK(cudaStreamWaitEvent(c->stream, f->ev, 0));
+}
+
 void check_field(const acg_context* c, const acg_field* f, const char* what) {
     if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "%s: null field", what);
     if (f->ctx != c && !(f->ctx && c && f->ctx->m == c->m && f->ctx->n_z == c->n_z &&
                          f->ctx->slabs.size() == c->slabs.size() && f->ctx->dtype == c->dtype))
         fail(ACG_ERR_INVALID_ARGUMENT, "%s: field does not match operator context", what);
+    await_field(c, f);
 }
 
 template <typename T>
@@ -517,6 +534,7 @@ void destroy_cached_solver(acg_context* c);  // defined after acg_solver
 void orphan_solver(acg_solver* s);           // frees a user solver's device state, ctx = NULL
 namespace {
 void free_pinned(const acg_context* c);      // pinned transfer chunks (defined with h2d/d2h)
+void release_field_memory(acg_field* f);  // device memory + async staging (after its transfers)
 }  // namespace
 
 // =================================================================== basics
@@ -704,8 +722,9 @@ acg_status acg_context_destroy(acg_context* c) {
         cudaStreamSynchronize(c->stream);
         for (acg_solver* us : c->user_solvers) orphan_solver(us);
         for (acg_field* f : c->user_fields) {
-            for (void* b : f->base) cudaFree(b);
-            f->base.clear();
+            release_field_memory(f);
+            if (f->ev) cudaEventDestroy(f->ev);
+            f->ev = nullptr;
             f->ctx = nullptr;
         }
         destroy_cached_solver(c);
@@ -719,6 +738,8 @@ acg_status acg_context_destroy(acg_context* c) {
         if (c->gather_send) cudaFree(c->gather_send);
         ipc_detach(c->ipc.get());
         if (c->halo_stream) cudaStreamDestroy(c->halo_stream);
+        if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+        if (c->ev_copy) cudaEventDestroy(c->ev_copy);
         if (c->ev_ready) cudaEventDestroy(c->ev_ready);
         if (c->ev_halo) cudaEventDestroy(c->ev_halo);
         if (c->stream) cudaStreamDestroy(c->stream);
@@ -755,6 +776,7 @@ acg_status acg_synchronize(const acg_context* c) {
         DeviceGuard g(c->device);
         CtxLock lk(c);
         CK(cudaStreamSynchronize(c->stream));
+        if (c->copy_stream) CK(cudaStreamSynchronize(c->copy_stream));
     });
 }
 
@@ -796,6 +818,11 @@ acg_status acg_context_release_scratch(const acg_context* cc) {
         CtxLock lk(cc);
         acg_context* c = const_cast<acg_context*>(cc);
         CK(cudaStreamSynchronize(c->stream));
+        if (c->copy_stream) CK(cudaStreamSynchronize(c->copy_stream));
+        for (acg_field* f : c->user_fields) {  // async-transfer staging
+            for (void* b : f->stage) cudaFree(b);
+            f->stage.clear();
+        }
         destroy_cached_solver(c);
         for (acg_field* f : c->pool) {
             for (void* b : f->base) cudaFree(b);
@@ -839,8 +866,19 @@ acg_field* new_field(const acg_context* c, bool zero_all = true) {
     return f.release();
 }
 
-void free_field(acg_field* f) {
+// Device memory of a field (its async transfers complete first).
+void release_field_memory(acg_field* f) {
+    if (f->ev) cudaEventSynchronize(f->ev);
     for (void* b : f->base) cudaFree(b);
+    f->base.clear();
+    for (void* b : f->stage) cudaFree(b);
+    f->stage.clear();
+    f->pending = false;
+}
+
+void free_field(acg_field* f) {
+    release_field_memory(f);
+    if (f->ev) cudaEventDestroy(f->ev);
     delete f;
 }
 
@@ -966,68 +1004,141 @@ void d2h(const acg_context* c, void* host, const void* dev, size_t n) {
     }
 }
 
+// Asynchronous transfers run on the context's copy stream (created on first
+// use) with the field's own staging, so they overlap the solver's kernels.
+cudaStream_t copy_stream(const acg_context* cc) {
+    acg_context* c = const_cast<acg_context*>(cc);
+    if (!c->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+    }
+    return c->copy_stream;
+}
+
+// The copy stream starts after the work enqueued on the context's stream so
+// far (earlier kernels may still read or write the field).
+cudaStream_t begin_async(const acg_field* f, const void* host, const char* what) {
+    const acg_context* c = f->ctx;
+    if (!host_is_pinned(host))
+        fail(ACG_ERR_INVALID_ARGUMENT,
+             "%s: the host buffer is not page-locked (acg_host_alloc / cudaHostAlloc / "
+             "cudaHostRegister); use the synchronous call for pageable memory", what);
+    cudaStream_t cs = copy_stream(c);
+    CK(cudaEventRecord(c->ev_copy, c->stream));
+    CK(cudaStreamWaitEvent(cs, c->ev_copy, 0));
+    if (!f->ev) CK(cudaEventCreateWithFlags(&f->ev, cudaEventDisableTiming));
+    if (f->stage.empty())
+        for (const Slab& sl : c->slabs) {
+            void* p = nullptr;
+            CK(cudaMalloc(&p, static_cast<size_t>(sl.n_loc) * c->s));
+            f->stage.push_back(p);
+        }
+    return cs;
+}
+
+// The copy engines serve the DMA commands of all streams in order: one 1 GB
+// command would hold the solver's small scalar reads (the done-flag polls,
+// history drains) for ~20 ms, so async transfers go in 8 MB pieces (~0.15 ms
+// each at PCIe 5 rates).
+void dma_chunked(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t st) {
+    constexpr size_t kChunk = size_t(8) << 20;
+    for (size_t off = 0; off < n; off += kChunk)
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                           std::min(kChunk, n - off), kind, st));
+}
+
+void end_async(const acg_field* f, cudaStream_t cs) {
+    CK(cudaEventRecord(f->ev, cs));
+    f->pending = true;
+}
+
+// Host -> field: the DMA into a staging buffer, then the relayout kernel. The
+// synchronous path (async = false) uses the context's stream and staging and
+// accepts pageable memory (h2d); the asynchronous one the copy stream and the
+// field's staging, with page-locked memory only.
 template <typename T>
-void upload_t(acg_field* f, const void* host, acg_layout layout, acg_host_scope scope) {
+void upload_t(acg_field* f, const void* host, acg_layout layout, acg_host_scope scope,
+              bool async = false) {
     const acg_context* c = f->ctx;
     const int m = c->m, n_z = c->n_z;
+    cudaStream_t st = async ? begin_async(f, host, "upload_async") : c->stream;
+    auto copy = [&](void* dst, const void* src, size_t n) {
+        if (async)
+            dma_chunked(dst, src, n, cudaMemcpyHostToDevice, st);
+        else
+            h2d(c, dst, src, n);
+    };
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& s = c->slabs[si];
-        T* st = static_cast<T*>(staging(c, si));
+        T* stg = static_cast<T*>(async ? f->stage[si] : staging(c, si));
         T* dst = static_cast<T*>(f->data(si));
         if (layout == ACG_LAYOUT_VERTICAL) {
             const T* src = static_cast<const T*>(host) +
                            (scope == ACG_HOST_FULL ? static_cast<size_t>(s.i0) * m * n_z : 0);
-            h2d(c, st, src, static_cast<size_t>(s.n_loc) * sizeof(T));
-            // st[(il*m + j)*n_z + k] -> dst[il*plane + k*m + j]
-            launch_transpose<T>(st, dst, n_z, m, s.m_loc, n_z, static_cast<long long>(m) * n_z, m,
-                                s.plane, c->stream);
+            copy(stg, src, static_cast<size_t>(s.n_loc) * sizeof(T));
+            // stg[(il*m + j)*n_z + k] -> dst[il*plane + k*m + j]
+            launch_transpose<T>(stg, dst, n_z, m, s.m_loc, n_z, static_cast<long long>(m) * n_z, m,
+                                s.plane, st);
         } else {
             if (scope == ACG_HOST_FULL && s.m_loc != m) {  // strided rows of this slab
-                CK(cudaMemcpy2DAsync(st, s.m_loc * sizeof(T),
+                CK(cudaMemcpy2DAsync(stg, s.m_loc * sizeof(T),
                                      static_cast<const T*>(host) + s.i0, m * sizeof(T),
                                      s.m_loc * sizeof(T), static_cast<size_t>(m) * n_z,
-                                     cudaMemcpyHostToDevice, c->stream));
+                                     cudaMemcpyHostToDevice, st));
             } else {
-                h2d(c, st, host, static_cast<size_t>(s.n_loc) * sizeof(T));
+                copy(stg, host, static_cast<size_t>(s.n_loc) * sizeof(T));
             }
-            // st[(j*n_z + k)*m_loc + il] -> dst[il*plane + k*m + j]
-            launch_transpose<T>(st, dst, s.m_loc, m, n_z, static_cast<long long>(n_z) * s.m_loc,
-                                s.m_loc, s.plane, m, c->stream);
+            // stg[(j*n_z + k)*m_loc + il] -> dst[il*plane + k*m + j]
+            launch_transpose<T>(stg, dst, s.m_loc, m, n_z, static_cast<long long>(n_z) * s.m_loc,
+                                s.m_loc, s.plane, m, st);
         }
         CK(cudaPeekAtLastError());
     }
+    if (async) end_async(f, st);
 }
 
+// Field -> host; the synchronous path returns with the host buffer complete,
+// the asynchronous one after enqueueing (acg_field_wait completes it).
 template <typename T>
-void download_t(const acg_field* f, void* host, acg_layout layout, acg_host_scope scope) {
+void download_t(const acg_field* f, void* host, acg_layout layout, acg_host_scope scope,
+                bool async = false) {
     const acg_context* c = f->ctx;
     const int m = c->m, n_z = c->n_z;
+    cudaStream_t st = async ? begin_async(f, host, "download_async") : c->stream;
+    auto copy = [&](void* dst, const void* src, size_t n) {
+        if (async)
+            dma_chunked(dst, src, n, cudaMemcpyDeviceToHost, st);
+        else
+            d2h(c, dst, src, n);
+    };
     for (size_t si = 0; si < c->slabs.size(); ++si) {
         const Slab& s = c->slabs[si];
-        T* st = static_cast<T*>(staging(c, si));
+        T* stg = static_cast<T*>(async ? f->stage[si] : staging(c, si));
         const T* src = static_cast<const T*>(f->data(si));
         if (layout == ACG_LAYOUT_VERTICAL) {
-            // src[il*plane + k*m + j] -> st[(il*m + j)*n_z + k]
-            launch_transpose<T>(src, st, m, n_z, s.m_loc, m, s.plane, n_z,
-                                static_cast<long long>(m) * n_z, c->stream);
+            // src[il*plane + k*m + j] -> stg[(il*m + j)*n_z + k]
+            launch_transpose<T>(src, stg, m, n_z, s.m_loc, m, s.plane, n_z,
+                                static_cast<long long>(m) * n_z, st);
             T* dst = static_cast<T*>(host) +
                      (scope == ACG_HOST_FULL ? static_cast<size_t>(s.i0) * m * n_z : 0);
-            d2h(c, dst, st, static_cast<size_t>(s.n_loc) * sizeof(T));
+            copy(dst, stg, static_cast<size_t>(s.n_loc) * sizeof(T));
         } else {
-            // src[il*plane + k*m + j] -> st[(j*n_z + k)*m_loc + il]
-            launch_transpose<T>(src, st, m, s.m_loc, n_z, s.plane, m,
-                                static_cast<long long>(n_z) * s.m_loc, s.m_loc, c->stream);
+            // src[il*plane + k*m + j] -> stg[(j*n_z + k)*m_loc + il]
+            launch_transpose<T>(src, stg, m, s.m_loc, n_z, s.plane, m,
+                                static_cast<long long>(n_z) * s.m_loc, s.m_loc, st);
             if (scope == ACG_HOST_FULL && s.m_loc != m) {
-                CK(cudaMemcpy2DAsync(static_cast<T*>(host) + s.i0, m * sizeof(T), st,
+                CK(cudaMemcpy2DAsync(static_cast<T*>(host) + s.i0, m * sizeof(T), stg,
                                      s.m_loc * sizeof(T), s.m_loc * sizeof(T),
-                                     static_cast<size_t>(m) * n_z, cudaMemcpyDeviceToHost,
-                                     c->stream));
+                                     static_cast<size_t>(m) * n_z, cudaMemcpyDeviceToHost, st));
             } else {
-                d2h(c, host, st, static_cast<size_t>(s.n_loc) * sizeof(T));
+                copy(host, stg, static_cast<size_t>(s.n_loc) * sizeof(T));
             }
         }
     }
-    CK(cudaStreamSynchronize(c->stream));
+    if (async)
+        end_async(f, st);
+    else
+        CK(cudaStreamSynchronize(c->stream));
 }
 
 // Device-resident counterparts (the Python edge hands over torch/CuPy device
@@ -1444,6 +1555,7 @@ acg_status acg_field_upload(acg_field* f, const void* host, acg_layout layout,
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, f);
         ACG_TDISPATCH(c, upload_t<T>(f, host, layout, scope));
     });
 }
@@ -1456,7 +1568,42 @@ acg_status acg_field_download(const acg_field* f, void* host, acg_layout layout,
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, f);
         ACG_TDISPATCH(c, download_t<T>(f, host, layout, scope));
+    });
+}
+
+acg_status acg_field_upload_async(acg_field* f, const void* host, acg_layout layout,
+                                  acg_host_scope scope) {
+    return guarded([&] {
+        if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
+        DeviceGuard g(c->device);
+        CtxLock lk(c);
+        ACG_TDISPATCH(c, upload_t<T>(f, host, layout, scope, true));
+    });
+}
+
+acg_status acg_field_download_async(const acg_field* f, void* host, acg_layout layout,
+                                    acg_host_scope scope) {
+    return guarded([&] {
+        if (!f || !host) fail(ACG_ERR_INVALID_ARGUMENT, "null argument");
+        const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
+        DeviceGuard g(c->device);
+        CtxLock lk(c);
+        ACG_TDISPATCH(c, download_t<T>(f, host, layout, scope, true));
+    });
+}
+
+acg_status acg_field_wait(const acg_field* f) {
+    return guarded([&] {
+        if (!f) fail(ACG_ERR_INVALID_ARGUMENT, "null field");
+        const acg_context* c = f->ctx;
+        if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
+        DeviceGuard g(c->device);
+        if (f->ev) CK(cudaEventSynchronize(f->ev));
     });
 }
 
@@ -1468,6 +1615,7 @@ acg_status acg_field_upload_device(acg_field* f, const void* dev, acg_layout lay
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, f);
         ACG_TDISPATCH(c, upload_dev_t<T>(f, dev, layout, scope));
     });
 }
@@ -1480,6 +1628,7 @@ acg_status acg_field_download_device(const acg_field* f, void* dev, acg_layout l
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, f);
         ACG_TDISPATCH(c, download_dev_t<T>(f, dev, layout, scope));
     });
 }
@@ -1491,6 +1640,7 @@ acg_status acg_field_fill(acg_field* f, double value) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, f);
         ACG_TDISPATCH(c, {
             for (size_t si = 0; si < c->slabs.size(); ++si)
                 launch_fill<T>(c->slabs[si].n_loc, static_cast<T>(value),
@@ -1507,6 +1657,7 @@ acg_status acg_field_fill_random(acg_field* f, uint64_t seed) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, f);
         ACG_TDISPATCH(c, {
             for (size_t si = 0; si < c->slabs.size(); ++si)
                 launch_fill_random<T>(view<T>(c, si), seed, static_cast<T*>(f->data(si)),
@@ -1523,6 +1674,8 @@ acg_status acg_field_copy(acg_field* dst, const acg_field* src) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, dst);
+        await_field(c, src);
         ACG_TDISPATCH(c, op_copy<T>(c, src, dst, nullptr));
         CK(cudaPeekAtLastError());
     });
@@ -1568,6 +1721,8 @@ acg_status acg_axpy(double alpha, const acg_field* x, acg_field* y) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, x);
+        await_field(c, y);
         ACG_TDISPATCH(c, op_axpy<T>(c, static_cast<T>(alpha), nullptr, -1, false, x, y, false));
         CK(cudaPeekAtLastError());
     });
@@ -1580,6 +1735,7 @@ acg_status acg_scal(double alpha, acg_field* x) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, x);
         ACG_TDISPATCH(c, {
             for (size_t si = 0; si < c->slabs.size(); ++si)
                 launch_scal<T>(c->slabs[si].n_loc, static_cast<T>(alpha), nullptr,
@@ -1597,6 +1753,8 @@ acg_status acg_dot(const acg_field* x, const acg_field* y, double* out) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, x);
+        await_field(c, y);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c);
             auto S = tmp_scalars<T>(c);
@@ -1613,6 +1771,7 @@ acg_status acg_nrm2(const acg_field* x, double* out) {
         if (!c) fail(ACG_ERR_INVALID_ARGUMENT, "field of a destroyed context");
         DeviceGuard g(c->device);
         CtxLock lk(c);
+        await_field(c, x);
         ACG_TDISPATCH(c, {
             reset_tmp<T>(c);
             auto S = tmp_scalars<T>(c);
@@ -1782,7 +1941,8 @@ struct acg_solver {
     const acg_field* f = nullptr;
     std::vector<void*> S;     // Scalars<T>* per local slab
     std::vector<double*> hist;  // 4 arrays per local slab
-    void* mirror = nullptr;   // pinned 2 x Scalars<T>
+    void* mirror = nullptr;   // pinned 2 x Scalars<T>, mapped
+    void* mirror_dev = nullptr;  // its device address (launch_snapshot target)
     cudaEvent_t mev[2] = {nullptr, nullptr};
     bool started = false;
     int cap = 0;              // device history ring capacity (entries, power of two)
@@ -1885,7 +2045,8 @@ void solver_alloc(acg_solver* s) {
         }
     }
     if (c->slabs.size() == 1) CK(cudaMalloc(&s->S_alt, sizeof(Scalars<T>)));
-    CK(cudaHostAlloc(&s->mirror, 2 * sizeof(Scalars<T>), cudaHostAllocPortable));
+    CK(cudaHostAlloc(&s->mirror, 2 * sizeof(Scalars<T>), cudaHostAllocPortable | cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&s->mirror_dev, s->mirror, 0));
     for (auto& e : s->mev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     s->u = new_field(c, false);
     s->r = new_field(c, false);
@@ -2325,9 +2486,13 @@ void solver_run(acg_solver* s) {
     int batch = static_cast<int>(std::ceil(1500.0 / est_us));
     batch = std::max(1, std::min(batch, 64));
     Scalars<T>* mir = static_cast<Scalars<T>*>(s->mirror);
+    Scalars<T>* mir_dev = static_cast<Scalars<T>*>(s->mirror_dev);
+    constexpr int kWords = static_cast<int>(sizeof(Scalars<T>) / 8);
     int enq = 0, b = 0;
-    // state after init
-    CK(cudaMemcpyAsync(&mir[1], s->S[0], sizeof(Scalars<T>), cudaMemcpyDeviceToHost, c->stream));
+    // state after init (snapshots by a kernel: a D2H copy here would sit in the
+    // copy engines' queue behind any asynchronous field transfer and hold the
+    // solver's stream)
+    launch_snapshot(s->S[0], &mir_dev[1], kWords, c->stream);
     CK(cudaEventRecord(s->mev[1], c->stream));
     CK(cudaEventSynchronize(s->mev[1]));
     if (mir[1].done) return;
@@ -2335,8 +2500,7 @@ void solver_run(acg_solver* s) {
         const int n = std::min(batch, s->cfg.maxiter - enq);
         solver_iterate<T>(s, n);
         enq += n;
-        CK(cudaMemcpyAsync(&mir[b & 1], s->S[0], sizeof(Scalars<T>), cudaMemcpyDeviceToHost,
-                           c->stream));
+        launch_snapshot(s->S[0], &mir_dev[b & 1], kWords, c->stream);
         CK(cudaEventRecord(s->mev[b & 1], c->stream));
         if (b > 0) {
             CK(cudaEventSynchronize(s->mev[(b - 1) & 1]));

@@ -74,7 +74,8 @@ def test_gpu_arm_json_line():
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] and cb["sample"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert d["gpu_launches"] >= 4 * d["steps"]
+    # two sweeps per iteration at least (C1: consumed reductions)
+    assert d["gpu_launches"] >= 2 * d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
 
