@@ -79,7 +79,43 @@ def main():
             if only is None or only == np.float64:
                 assert np.array_equal(acg.random_field(m, n_z, 42), o.random_field(42))
         print(f"case {m}x{n_z} ok", flush=True)
+    async_transfers()
     print("SANITIZE_DONE", flush=True)
+
+
+def async_transfers():
+    """Copy-stream transfers overlapping a solve (upload_async of the next
+    right-hand side, download_async of the previous solution), both layouts.
+    Columns taller than TMEM holds (k_thomas), so synccheck can run it too."""
+    from paper_1302_7193_b200 import capi
+    nz = 272
+    prob = Problem(32, nz)
+    o = Oracle(prob)
+    ctx = capi.Context(o.ap, o.bp, o.cp, o.d, o.area, o.east, o.north, o.diag)
+    shape = (32, 32, nz)
+    hf = [capi.HostBuffer(shape) for _ in range(2)]
+    hu = [capi.HostBuffer(shape) for _ in range(2)]
+    for i, h in enumerate(hf):
+        h.array[...] = o.random_field(40 + i)
+    fs, us = [ctx.field(), ctx.field()], [ctx.field(), ctx.field()]
+    fs[0].upload_async(hf[0].array)
+    for i in range(2):
+        if i == 0:
+            fs[1].upload_async(hf[1].array, layout=capi.VERTICAL)
+        capi.solve(ctx, fs[i], u_out=us[i], epsilon=1e-9, maxiter=60)
+        us[i].download_async(hu[i].array)
+    for i in range(2):
+        us[i].wait()
+        uo, _ = o.solve(hf[i].array.copy(), epsilon=1e-9, maxiter=60)
+        assert np.array_equal(hu[i].array, uo)
+    h2 = capi.HostBuffer((32, nz, 32))
+    us[0].download_async(h2.array, layout=capi.HORIZONTAL)
+    us[0].wait()
+    assert np.array_equal(h2.array, np.ascontiguousarray(hu[0].array.transpose(1, 2, 0)))
+    for x in fs + us + hf + hu + [h2]:
+        x.close()
+    ctx.close()
+    print("async transfers ok", flush=True)
 
 
 if __name__ == "__main__":
