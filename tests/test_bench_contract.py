@@ -94,9 +94,11 @@ def test_gpu_arm_multi_rank_reexec(n, config):
         pytest.skip("no torch")
     env = dict(os.environ, OMP_NUM_THREADS="2", ACG_SAME_GPU="1")
     env.pop("WORLD_SIZE", None)
+    # the 2-rank run also times the e2e stream (async transfers on every rank)
+    extra = [] if n == 2 else ["--no-e2e"]
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n),
                         "--config", config, "--steps", "5", "--warmup", "3", "--no-cpu",
-                        "--no-e2e", "--sustain-steps", "20"],
+                        "--sustain-steps", "20"] + extra,
                        capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
@@ -106,3 +108,6 @@ def test_gpu_arm_multi_rank_reexec(n, config):
     v = d["verified_vs_1gpu"]
     assert v["ok"] is True and v["exact_tree"] is True and v["max_dev_over_r0"] == 0.0
     assert d["sustained"]["steps"] == 20 and d["sustained"]["value"] > 0
+    if n == 2:
+        e = d["e2e"]
+        assert e["value"] > 0 and e["solves"] >= 2 and e["serial"]["value"] > 0
