@@ -412,58 +412,58 @@ __global__ void __launch_bounds__(32 * kStencilWarps, MINB)
             alpha = cr.alpha;
             beta = cr.beta;
         }
-        if (!valid) goto swept;
-        P z0{T(0), T(0)}, zd{T(0), T(0)};
-        if (k0 < k1) {
-            z0 = *reinterpret_cast<const P*>(zc + static_cast<long long>(k0) * sm);
-            zd = k0 > 0 ? *reinterpret_cast<const P*>(zc + static_cast<long long>(k0 - 1) * sm) : z0;
-        }
-        const int len = KS ? (n_z + kseg - 1) / kseg : 0;  // KS: group 0's level count
-        int cs = 0, ps_ = D;
-        for (int k = k0; k < k1; ++k) {
-            const long long l = static_cast<long long>(k) * sm;
-            cp_wait<D - 1>();
-            const P* r0 = ring + cs * 7 * NT;
-            P pv = r0[0], qv = r0[NT];
-            const P uv = r0[2 * NT];
-            const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
-            const P ce = r0[4 * NT], cw = r0[5 * NT];
-            const P ex = r0[6 * NT];
-            const T cs0 = ex.x, cn1 = ex.y;
-            if (k + D < k1) issue(k + D, ps_);
-            cp_commit();
-            cs = cs + 1 == NS ? 0 : cs + 1;
-            ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
-            const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
-            pv.x = A::add(A::mul(beta, pv.x), z0.x);
-            pv.y = A::add(A::mul(beta, pv.y), z0.y);
-            qv.x = A::mul(beta, qv.x);
-            qv.y = A::mul(beta, qv.y);
-            // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
-            const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
-                                           ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
-            // column j+1: south = own .x, north = z(j+2) (own value on the edge)
-            const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
-                                           cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
-            qv.x = A::add(qv.x, A::mul(dP[k], dqa));
-            qv.y = A::add(qv.y, A::mul(dP[k], dqb));
-            if (KS && grp > 0) {
-                prod[(k - len) * (m >> 1) + (j >> 1)] = P{A::mul(pv.x, qv.x), A::mul(pv.y, qv.y)};
-            } else {
-                siga = A::add(siga, A::mul(pv.x, qv.x));
-                sigb = A::add(sigb, A::mul(pv.y, qv.y));
+        if (valid) {
+            P z0{T(0), T(0)}, zd{T(0), T(0)};
+            if (k0 < k1) {
+                z0 = *reinterpret_cast<const P*>(zc + static_cast<long long>(k0) * sm);
+                zd = k0 > 0 ? *reinterpret_cast<const P*>(zc + static_cast<long long>(k0 - 1) * sm) : z0;
             }
-            if (valid) {
-                st_pair_cs(uc + l, un);
-                st_pair_cs(pc + l, pv);
-                st_pair_cs(qc + l, qv);
+            const int len = KS ? (n_z + kseg - 1) / kseg : 0;  // KS: group 0's level count
+            int cur = 0, ps_ = D;
+            for (int k = k0; k < k1; ++k) {
+                const long long l = static_cast<long long>(k) * sm;
+                cp_wait<D - 1>();
+                const P* r0 = ring + cur * 7 * NT;
+                P pv = r0[0], qv = r0[NT];
+                const P uv = r0[2 * NT];
+                const P zu = k + 1 < n_z ? r0[3 * NT] : z0;
+                const P ce = r0[4 * NT], cw = r0[5 * NT];
+                const P ex = r0[6 * NT];
+                const T cs0 = ex.x, cn1 = ex.y;
+                if (k + D < k1) issue(k + D, ps_);
+                cp_commit();
+                cur = cur + 1 == NS ? 0 : cur + 1;
+                ps_ = ps_ + 1 == NS ? 0 : ps_ + 1;
+                const P un{A::add(uv.x, A::mul(alpha, pv.x)), A::add(uv.y, A::mul(alpha, pv.y))};
+                pv.x = A::add(A::mul(beta, pv.x), z0.x);
+                pv.y = A::add(A::mul(beta, pv.y), z0.y);
+                qv.x = A::mul(beta, qv.x);
+                qv.y = A::mul(beta, qv.y);
+                // column j: north = own .y (exists: m even), south = z(j-1) (own value on the edge)
+                const T dqa = stencil<T, Fast>(sP[k], ca.area, ca.adiag, bP[k], cP[k], ca.ae, ca.aw, ca.an,
+                                               ca.as, z0.x, zu.x, zd.x, ce.x, cw.x, z0.y, cs0);
+                // column j+1: south = own .x, north = z(j+2) (own value on the edge)
+                const T dqb = stencil<T, Fast>(sP[k], cb.area, cb.adiag, bP[k], cP[k], cb.ae, cb.aw, cb.an,
+                                               cb.as, z0.y, zu.y, zd.y, ce.y, cw.y, cn1, z0.x);
+                qv.x = A::add(qv.x, A::mul(dP[k], dqa));
+                qv.y = A::add(qv.y, A::mul(dP[k], dqb));
+                if (KS && grp > 0) {
+                    prod[(k - len) * (m >> 1) + (j >> 1)] = P{A::mul(pv.x, qv.x), A::mul(pv.y, qv.y)};
+                } else {
+                    siga = A::add(siga, A::mul(pv.x, qv.x));
+                    sigb = A::add(sigb, A::mul(pv.y, qv.y));
+                }
+                if (valid) {
+                    st_pair_cs(uc + l, un);
+                    st_pair_cs(pc + l, pv);
+                    st_pair_cs(qc + l, qv);
+                }
+                zd = z0;
+                z0 = zu;
             }
-            zd = z0;
-            z0 = zu;
+            cp_wait<0>();
         }
-        cp_wait<0>();
     }
-swept:
     if constexpr (KS) {  // group 0 carries the running sums through the later levels
         __syncthreads();
         if (grp == 0) {
