@@ -25,7 +25,7 @@ CostReport cost_model(Kernel kernel, CacheAssumption cache);
 CostReport blas_op_cost(BlasOp op);
 /// flops * points / seconds and mem_refs * points * scalar_bytes / seconds
 ThroughputEstimate throughput_estimate(const CostReport& report, std::int64_t grid_points,
-                                       double seconds, int scalar_bytes);
+                                       double seconds, int scalar_bytes = 8);
 
 std::string_view to_string(Kernel kernel);
 std::string_view to_string(CacheAssumption cache);

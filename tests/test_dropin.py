@@ -12,6 +12,12 @@ tests then run verbatim twice:
 
 On a machine without a GPU only the host-only tests are run (setup and cost
 tables); compute calls must fail loudly there, never fall back.
+
+The same holds one level down: the reference's own C++ unit tests
+(proj/tests/test_{field,grid,profile,operator,solver,cost_model}.cpp with
+its oracles.hpp), compiled UNMODIFIED against include/anisocg/*.hpp and linked
+to libacg_cuda.so (oracle/_ref/cpptests/, with tests/refcpp/doctest.h standing
+in for the absent doctest header), must pass all 59 test cases on the GPU.
 """
 import hashlib
 import os
@@ -87,3 +93,17 @@ def test_reference_smoke_all_eleven(module):
     r = run_smoke(where, path)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "11 passed" in r.stdout, r.stdout[-2000:]
+
+
+CPPTESTS = os.path.join(ROOT, "oracle", "_ref", "cpptests", "ref_unit_tests")
+
+
+@pytest.mark.gpu
+def test_reference_cpp_unit_tests_all_pass():
+    if not os.path.exists(CPPTESTS):
+        pytest.skip("oracle/_ref/cpptests not built (needs /root/reference at build time)")
+    r = subprocess.run([CPPTESTS], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    summary = [l for l in r.stdout.splitlines() if l.startswith("[refcpp]")]
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert summary and "| 59 passed | 0 failed |" in summary[-1], r.stdout[-3000:]
+    assert summary[-1].rstrip().endswith("| 0 failed"), summary[-1]
