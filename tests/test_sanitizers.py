@@ -106,3 +106,20 @@ def test_synccheck_rejects_bare_tmem_alloc():
     # recorded either way; the test documents which it is on this toolkit
     print("synccheck on a bare TMEM alloc/dealloc:",
           "flags it" if "Barrier error" in r.stdout + r.stderr else "accepts it")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "initcheck"])
+def test_reference_cpp_unit_tests_clean(tool):
+    """The reference's own C++ unit tests (59 cases through the drop-in C++
+    API: host shim, C ABI, every operator and solver entry point) under the
+    sanitizer: all pass and no errors."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "cpptests", "ref_unit_tests")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/cpptests not built (needs /root/reference at build time)")
+    r = subprocess.run([sanitizer(), "--tool", tool, "--error-exitcode", "97", "--print-limit", "50",
+                        exe], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    log = r.stdout + r.stderr
+    keep_log(f"refcpp_{tool}", log)
+    assert r.returncode == 0, log[-4000:]
+    assert "| 59 passed | 0 failed |" in log, log[-3000:]
+    assert clean(log, 1), log[-4000:]
