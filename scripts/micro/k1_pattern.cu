@@ -1,0 +1,114 @@
+// K1's memory pattern without its arithmetic: how fast can the exact sweep's
+// traffic go at the occupancy the real kernel has? C3 (1024^2 x 128 fp64,
+// plane-major [il][k][j]): one thread per column, CTA = one plane x 128 j,
+// 4 planes per CTA; forward reads r, q through a 16-slot cp.async ring 15
+// levels ahead and writes r* = r - alpha q; backward re-reads r* top-down
+// through the ring (L2) and writes z = r* + 0.5 z_{k+1}. Dynamic shared
+// memory is padded to hold `ctas` CTAs per SM (k_thomas_tm: 2, by TMEM).
+// Prints ms per launch (CUDA events, 20 launches after 3 warm-up) and the
+// algorithmic 4.31 GB model rate.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o k1_pattern k1_pattern.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+constexpr int M = 1024, NZ = 128, NT = 128, NS = 16, D = 15, TPC = 4;
+
+__device__ __forceinline__ void cpa8(double* s, const double* g) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void wait_g() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const double* __restrict__ q,
+                                                 double* __restrict__ z, double alpha) {
+    extern __shared__ double ring_all[];  // [slot][2][NT]
+    const int tid = threadIdx.x;
+    double* ring = ring_all + tid;
+    const long long plane = static_cast<long long>(NZ) * M;
+    for (int rep = 0; rep < TPC; ++rep) {
+        const int il = blockIdx.y * TPC + rep;
+        const int j = blockIdx.x * NT + tid;
+        double* rc = r + il * plane + j;
+        const double* qc = q + il * plane + j;
+        double* zc = z + il * plane + j;
+        for (int t = 0; t < D; ++t) {
+            cpa8(ring + (2 * t) * NT, rc + static_cast<long long>(t) * M);
+            cpa8(ring + (2 * t + 1) * NT, qc + static_cast<long long>(t) * M);
+            commit();
+        }
+        double top = 0.0;
+        for (int k = 0; k < NZ; ++k) {
+            wait_g<D - 1>();
+            const double rv = ring[(2 * (k % NS)) * NT], qv = ring[(2 * (k % NS) + 1) * NT];
+            if (k + D < NZ) {
+                cpa8(ring + (2 * ((k + D) % NS)) * NT, rc + static_cast<long long>(k + D) * M);
+                cpa8(ring + (2 * ((k + D) % NS) + 1) * NT, qc + static_cast<long long>(k + D) * M);
+            }
+            commit();
+            const double rs = rv - alpha * qv;
+            rc[static_cast<long long>(k) * M] = rs;
+            top = rs;
+        }
+        wait_g<0>();
+        __threadfence_block();
+        for (int t = 0; t < D; ++t) {
+            const int k = NZ - 2 - t;
+            if (k >= 0) cpa8(ring + (2 * (k % NS)) * NT, rc + static_cast<long long>(k) * M);
+            commit();
+        }
+        double zn = top;
+        zc[static_cast<long long>(NZ - 1) * M] = zn;
+        for (int k = NZ - 2; k >= 0; --k) {
+            wait_g<D - 1>();
+            const double rk = ring[(2 * (k % NS)) * NT];
+            if (k - D >= 0) cpa8(ring + (2 * ((k - D) % NS)) * NT, rc + static_cast<long long>(k - D) * M);
+            commit();
+            zn = rk + 0.5 * zn;
+            zc[static_cast<long long>(k) * M] = zn;
+        }
+        wait_g<0>();
+        __syncthreads();
+    }
+}
+
+int main() {
+    const size_t n = static_cast<size_t>(M) * M * NZ;
+    double *r, *q, *z;
+    cudaMalloc(&r, n * 8);
+    cudaMalloc(&q, n * 8);
+    cudaMalloc(&z, n * 8);
+    cudaMemset(r, 0, n * 8);
+    cudaMemset(q, 0, n * 8);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const dim3 grid(M / NT, M / TPC), block(NT);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int ctas : {2, 3, 4}) {
+        size_t smem = 233472 / (ctas + 1) - 1024 + 64;  // the k_thomas_tm padding rule
+        const size_t ring = static_cast<size_t>(NS) * 2 * NT * 8;
+        if (smem < ring) smem = ring;
+        cudaFuncSetAttribute(k_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pattern, NT, smem);
+        for (int i = 0; i < 3; ++i) k_pattern<<<grid, block, smem>>>(r, q, z, 0.37);
+        cudaEventRecord(e0);
+        for (int i = 0; i < 20; ++i) k_pattern<<<grid, block, smem>>>(r, q, z, 0.37);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 20;
+        const double model = 4.0 * n * 8 + 2.0 * M * M * 8;  // K1's algorithmic bytes
+        std::printf("CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the 4.31 GB model\n",
+                    ctas, occ, occ * 4, ms, model / ms / 1e6);
+    }
+    std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
+}
