@@ -24,6 +24,10 @@ __device__ __forceinline__ void wait_g() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// DEFER: the z stores of plane p move into the forward sweep of plane p + 1
+// (k_thomas_tm would read them back from TMEM), so both phases mix reads and
+// writes; the CTA's last plane flushes its z after its backward sweep.
+template <bool DEFER>
 __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const double* __restrict__ q,
                                                  double* __restrict__ z, double alpha) {
     extern __shared__ double ring_all[];  // [slot][2][NT]
@@ -42,6 +46,7 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
             commit();
         }
         double top = 0.0;
+        double* zprev = z + (il - 1) * plane + j;  // DEFER: the previous plane's z
         for (int k = 0; k < NZ; ++k) {
             wait_g<D - 1>();
             const double rv = ring[(2 * (k % NS)) * NT], qv = ring[(2 * (k % NS) + 1) * NT];
@@ -52,6 +57,7 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
             commit();
             const double rs = rv - alpha * qv;
             rc[static_cast<long long>(k) * M] = rs;
+            if (DEFER && rep > 0) zprev[static_cast<long long>(k) * M] = rs * 0.25;
             top = rs;
         }
         wait_g<0>();
@@ -62,14 +68,14 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
             commit();
         }
         double zn = top;
-        zc[static_cast<long long>(NZ - 1) * M] = zn;
+        if (!DEFER || rep == TPC - 1) zc[static_cast<long long>(NZ - 1) * M] = zn;
         for (int k = NZ - 2; k >= 0; --k) {
             wait_g<D - 1>();
             const double rk = ring[(2 * (k % NS)) * NT];
             if (k - D >= 0) cpa8(ring + (2 * ((k - D) % NS)) * NT, rc + static_cast<long long>(k - D) * M);
             commit();
             zn = rk + 0.5 * zn;
-            zc[static_cast<long long>(k) * M] = zn;
+            if (!DEFER || rep == TPC - 1) zc[static_cast<long long>(k) * M] = zn;
         }
         wait_g<0>();
         __syncthreads();
@@ -90,24 +96,26 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+    for (int defer = 0; defer < 2; ++defer)
     for (int ctas : {2, 3, 4}) {
+        auto kern = defer ? k_pattern<true> : k_pattern<false>;
         size_t smem = 233472 / (ctas + 1) - 1024 + 64;  // the k_thomas_tm padding rule
         const size_t ring = static_cast<size_t>(NS) * 2 * NT * 8;
         if (smem < ring) smem = ring;
-        cudaFuncSetAttribute(k_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pattern, NT, smem);
-        for (int i = 0; i < 3; ++i) k_pattern<<<grid, block, smem>>>(r, q, z, 0.37);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+        for (int i = 0; i < 3; ++i) kern<<<grid, block, smem>>>(r, q, z, 0.37);
         cudaEventRecord(e0);
-        for (int i = 0; i < 20; ++i) k_pattern<<<grid, block, smem>>>(r, q, z, 0.37);
+        for (int i = 0; i < 20; ++i) kern<<<grid, block, smem>>>(r, q, z, 0.37);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         ms /= 20;
         const double model = 4.0 * n * 8 + 2.0 * M * M * 8;  // K1's algorithmic bytes
-        std::printf("CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the 4.31 GB model\n",
-                    ctas, occ, occ * 4, ms, model / ms / 1e6);
+        std::printf("%s CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the 4.31 GB model\n",
+                    defer ? "deferred z:" : "as K1:     ", ctas, occ, occ * 4, ms, model / ms / 1e6);
     }
     std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
