@@ -27,7 +27,9 @@ __device__ __forceinline__ void wait_g() {
 // DEFER: the z stores of plane p move into the forward sweep of plane p + 1
 // (k_thomas_tm would read them back from TMEM), so both phases mix reads and
 // writes; the CTA's last plane flushes its z after its backward sweep.
-template <bool DEFER>
+// TOPREG: the backward sweep takes the top 16 levels' r* from registers (kept
+// from the end of the forward sweep) and re-reads only the levels below.
+template <bool DEFER, bool TOPREG = false>
 __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const double* __restrict__ q,
                                                  double* __restrict__ z, double alpha) {
     extern __shared__ double ring_all[];  // [slot][2][NT]
@@ -46,6 +48,7 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
             commit();
         }
         double top = 0.0;
+        double keep[16];
         double* zprev = z + (il - 1) * plane + j;  // DEFER: the previous plane's z
         for (int k = 0; k < NZ; ++k) {
             wait_g<D - 1>();
@@ -58,18 +61,27 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
             const double rs = rv - alpha * qv;
             rc[static_cast<long long>(k) * M] = rs;
             if (DEFER && rep > 0) zprev[static_cast<long long>(k) * M] = rs * 0.25;
+            if (TOPREG && k >= NZ - 16) keep[k - (NZ - 16)] = rs;
             top = rs;
         }
         wait_g<0>();
         __threadfence_block();
+        const int kb = TOPREG ? NZ - 17 : NZ - 2;  // first level re-read from memory
         for (int t = 0; t < D; ++t) {
-            const int k = NZ - 2 - t;
+            const int k = kb - t;
             if (k >= 0) cpa8(ring + (2 * (k % NS)) * NT, rc + static_cast<long long>(k) * M);
             commit();
         }
         double zn = top;
         if (!DEFER || rep == TPC - 1) zc[static_cast<long long>(NZ - 1) * M] = zn;
-        for (int k = NZ - 2; k >= 0; --k) {
+        if (TOPREG) {
+#pragma unroll
+            for (int k = NZ - 2; k > NZ - 17; --k) {
+                zn = keep[k - (NZ - 16)] + 0.5 * zn;
+                if (!DEFER || rep == TPC - 1) zc[static_cast<long long>(k) * M] = zn;
+            }
+        }
+        for (int k = kb; k >= 0; --k) {
             wait_g<D - 1>();
             const double rk = ring[(2 * (k % NS)) * NT];
             if (k - D >= 0) cpa8(ring + (2 * ((k - D) % NS)) * NT, rc + static_cast<long long>(k - D) * M);
@@ -96,9 +108,9 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int defer = 0; defer < 2; ++defer)
+    for (int defer = 0; defer < 3; ++defer)
     for (int ctas : {2, 3, 4}) {
-        auto kern = defer ? k_pattern<true> : k_pattern<false>;
+        auto kern = defer == 2 ? k_pattern<false, true> : defer ? k_pattern<true> : k_pattern<false>;
         size_t smem = 233472 / (ctas + 1) - 1024 + 64;  // the k_thomas_tm padding rule
         const size_t ring = static_cast<size_t>(NS) * 2 * NT * 8;
         if (smem < ring) smem = ring;
@@ -115,7 +127,7 @@ int main() {
         ms /= 20;
         const double model = 4.0 * n * 8 + 2.0 * M * M * 8;  // K1's algorithmic bytes
         std::printf("%s CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the 4.31 GB model\n",
-                    defer ? "deferred z:" : "as K1:     ", ctas, occ, occ * 4, ms, model / ms / 1e6);
+                    defer == 2 ? "top r* reg:" : defer ? "deferred z:" : "as K1:     ", ctas, occ, occ * 4, ms, model / ms / 1e6);
     }
     std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
