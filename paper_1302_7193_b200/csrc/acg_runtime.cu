@@ -2359,7 +2359,7 @@ double bytes_per_iteration(const acg_context* c);
 
 // Small grids replay a CUDA graph of kGraphChunk iterations instead of
 // launching 4-5 kernels per iteration from the host: C1 (128^2 x 64) 45.1 ->
-// 41.6 us per iteration; no change at C2/C3 (measured in round 2 with a since-removed switch), so
+// 41.6 us per iteration; no change at C2/C3 (an A/B switch, since removed), so
 // graphs are used below ~80 us of HBM traffic per iteration. Replay applies
 // where every launch of an iteration is the same from one iteration to the
 // next: one process (the peer-memory and NCCL transports put per-iteration
