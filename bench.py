@@ -516,10 +516,17 @@ def run_gpu(args, cfg):
         fs, us = [ctx.field(), ctx.field()], [ctx.field(), ctx.field()]
         kw = dict(epsilon=1e-300, tau=1e-300, maxiter=args.steps, variant=variant,
                   backend=backend)
-        # one untimed warm-up call (allocates the context's cached solver state)
+        # untimed warm-up: the context's cached solver state, and one asynchronous
+        # round trip per field (allocates each field's transfer staging once)
         fs[0].upload(hf[0].array, scope=capi.HOST_LOCAL)
         capi.solve(ctx, fs[0], u_out=us[0], **kw)
         us[0].download(out=hu[0].array, scope=capi.HOST_LOCAL)
+        for x, hx in ((fs[0], hf[0]), (fs[1], hf[1])):
+            x.upload_async(hx.array, scope=capi.HOST_LOCAL)
+        for x, hx in ((us[0], hu[0]), (us[1], hu[1])):
+            x.download_async(hx.array, scope=capi.HOST_LOCAL)
+        for x in fs + us:
+            x.wait()
         barrier()
         t0 = time.perf_counter()
         fs[0].upload(hf[0].array, scope=capi.HOST_LOCAL)
@@ -571,11 +578,32 @@ def run_gpu(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
+        # ~15 s of host work (the reference runs ~1.1 ns per point and iteration on
+        # 16 cores), at most 100 iterations: a sample long enough that the solve's
+        # first-touch of its five work fields does not dominate the rate
+        n_pts = cfg["m"] * cfg["m"] * cfg["n_z"]
+        cpu_iters = args.cpu_iters or int(min(100, max(5, round(15.0 / (n_pts * 1.1e-9)))))
         try:
-            r = cpu_reference(cfg, args.cpu_iters, cores)
+            # in a fresh process, exactly like the reference arm (this process holds
+            # the GPU context, pinned buffers and its own threads)
+            r = None
+            try:
+                cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference",
+                       "--config", args.config, "--steps", str(cpu_iters), "--warmup", "1"]
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                                     env={k: v for k, v in os.environ.items()
+                                          if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
+                line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
+                d = json.loads(line)
+                if d.get("cpu_baseline", {}).get("kind") == "reference":
+                    r = {"it_s": d["value"], "loop_s": cpu_iters / d["value"]}
+            except Exception:
+                r = None
+            if r is None:
+                r = cpu_reference(cfg, cpu_iters, cores)
             cpu = {"value": r["it_s"], "unit": "iter/s", "cores": cores, "kind": "reference",
                    "cpu_model": cpu_model(),
-                   "sample": f"{args.cpu_iters} interleaved iterations of the full "
+                   "sample": f"{cpu_iters} interleaved iterations of the full "
                              f"{cfg['m']}^2x{cfg['n_z']} {cfg['dtype']} problem, steady loop "
                              f"time from the reference's KernelTimings ({r['loop_s']:.1f} s)"}
         except Exception as exc:
@@ -622,7 +650,8 @@ def main():
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 halo/reduction transport: peer-memory mailboxes (CUDA IPC over "
                          "NVLink) or NCCL send/recv + all-gather")
-    ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--cpu-iters", type=int, default=0,
+                    help="iterations of the CPU baseline sample (0: ~15 s of host work, <= 100)")
     ap.add_argument("--sustain-steps", type=int, default=500,
                     help="iterations of the sustained (power-capped) pass reported beside the "
                          "headline (0: skip)")
