@@ -11,8 +11,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
-constexpr int M = 1024, NZ = 128, NT = 128, NS = 16, D = 15, TPC = 4;
+constexpr int NZ = 128, NT = 128, NS = 16, D = 15;
+__constant__ int cM, cTPC;  // panel width, planes per CTA (argv)
 
 __device__ __forceinline__ void cpa8(double* s, const double* g) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
@@ -35,9 +37,11 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
     extern __shared__ double ring_all[];  // [slot][2][NT]
     const int tid = threadIdx.x;
     double* ring = ring_all + tid;
+    const int M = cM, TPC = cTPC;
     const long long plane = static_cast<long long>(NZ) * M;
     for (int rep = 0; rep < TPC; ++rep) {
         const int il = blockIdx.y * TPC + rep;
+        if (il >= static_cast<int>(gridDim.y) * TPC || il >= M) break;
         const int j = blockIdx.x * NT + tid;
         double* rc = r + il * plane + j;
         const double* qc = q + il * plane + j;
@@ -94,7 +98,11 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const int M = argc > 1 ? std::atoi(argv[1]) : 1024, TPC = argc > 2 ? std::atoi(argv[2]) : 4;
+    cudaMemcpyToSymbol(cM, &M, sizeof(int));
+    cudaMemcpyToSymbol(cTPC, &TPC, sizeof(int));
+    std::printf("m = %d, n_z = %d, %d planes per CTA\n", M, NZ, TPC);
     const size_t n = static_cast<size_t>(M) * M * NZ;
     double *r, *q, *z;
     cudaMalloc(&r, n * 8);
@@ -104,7 +112,7 @@ int main() {
     cudaMemset(q, 0, n * 8);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const dim3 grid(M / NT, M / TPC), block(NT);
+    const dim3 grid(M / NT, (M + TPC - 1) / TPC), block(NT);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -126,7 +134,7 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         ms /= 20;
         const double model = 4.0 * n * 8 + 2.0 * M * M * 8;  // K1's algorithmic bytes
-        std::printf("%s CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the 4.31 GB model\n",
+        std::printf("%s CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the model\n",
                     defer == 2 ? "top r* reg:" : defer ? "deferred z:" : "as K1:     ", ctas, occ, occ * 4, ms, model / ms / 1e6);
     }
     std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
