@@ -93,3 +93,33 @@ def test_compute_fails_loudly_without_gpu(acg):
         acg.OperatorContext(acg.vertical_profile(g, 6.71e-4, 3.32e-2), acg.cubed_sphere_panel(2))
     with pytest.raises(RuntimeError):
         acg.random_field(2, 4, 1)
+
+
+def test_parallel_hpp_pairwise_sum_matches_the_oracle(tmp_path):
+    """include/anisocg/parallel.hpp (host pairwise_sum, parallel.hpp:11-20 of the
+    reference) sums in the same fixed tree as the oracle's restatement."""
+    import shutil
+    import subprocess
+    from oracle.oracle import Oracle, Problem
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not installed")
+    src = tmp_path / "ps.cpp"
+    src.write_text(
+        '#include <cstdio>\n#include <vector>\n#include "anisocg/parallel.hpp"\n'
+        "int main() { std::size_t n; std::vector<double> v;\n"
+        '  while (std::scanf("%zu", &n) == 1) { v.resize(n);\n'
+        '    for (auto& x : v) std::scanf("%la", &x);\n'
+        '    std::printf("%a\\n", anisocg::pairwise_sum(v.data(), v.size())); } }\n')
+    exe = tmp_path / "ps"
+    subprocess.run([gxx, "-O2", "-std=c++20", "-ffp-contract=off", "-I",
+                    os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    rng = np.random.default_rng(7)
+    sizes = [0, 1, 7, 8, 9, 16, 17, 100, 1023, 4096, 65537]
+    arrays = [rng.standard_normal(n) * 10.0 ** rng.integers(-8, 8, n) for n in sizes]
+    inp = "".join(f"{a.size}\n" + "".join(f"{float(x).hex()}\n" for x in a) for a in arrays)
+    out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True)
+    got = [float.fromhex(l) for l in out.stdout.split()]
+    o = Oracle(Problem(4, 2))
+    want = [o.pairwise_sum(a) if a.size else 0.0 for a in arrays]
+    assert got == want
