@@ -5,7 +5,7 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 timeout 2400 python -m pytest tests -m gpu -q --durations=30 > gpurun_out/pytest_gpu.log 2>&1
 echo "gpu suite rc=$?"; tail -8 gpurun_out/pytest_gpu.log
-for v in "base:" "ctafin:ACG_CTA_FINISH=1" "nopdl:ACG_PDL=0"; do
+for v in "base:" "nopdl:ACG_PDL=0"; do
   tag=${v%%:*}; envs=${v#*:}
   env $envs timeout 300 python bench.py --config c1 --steps 2000 --warmup 20 --no-cpu --no-e2e \
       --sustain-steps 0 > gpurun_out/c1_$tag.json 2> gpurun_out/c1_$tag.err
