@@ -112,3 +112,33 @@ def test_pageable_host_buffer_rejected():
         f.upload_async(np.zeros((32, 32, 8)))
     f.close()
     ctx.close()
+
+
+def test_async_edges():
+    """wait() without transfers returns at once; shape and dtype are checked
+    before anything is enqueued; release_scratch frees the staging and the
+    next transfer allocates it again; a field destroyed with a transfer in
+    flight waits for it."""
+    from paper_1302_7193_b200 import capi
+    prob = Problem(48, 10)
+    o, ctx = _ctx(capi, prob)
+    f = ctx.field()
+    f.wait()
+    hb = capi.HostBuffer((48, 48, 10), np.float64)
+    hb.array[...] = o.random_field(3)
+    with pytest.raises(ValueError):
+        f.upload_async(capi.HostBuffer((48, 10, 48), np.float64).array)
+    with pytest.raises(ValueError):
+        f.download_async(np.zeros((48, 48, 10), dtype=np.float32))
+    f.upload_async(hb.array)
+    ctx.release_scratch()  # synchronises the copy stream, frees the staging
+    assert np.array_equal(f.download(), hb.array)
+    out = capi.HostBuffer((48, 48, 10), np.float64)
+    f.download_async(out.array)  # staging re-created
+    f.wait()
+    assert np.array_equal(out.array, hb.array)
+    g = ctx.field()
+    g.upload_async(hb.array)
+    g.close()  # waits for its transfer before freeing
+    f.close()
+    ctx.close()
