@@ -31,12 +31,17 @@ __device__ __forceinline__ void wait_g() {
 // writes; the CTA's last plane flushes its z after its backward sweep.
 // TOPREG: the backward sweep takes the top 16 levels' r* from registers (kept
 // from the end of the forward sweep) and re-reads only the levels below.
-template <bool DEFER, bool TOPREG = false>
+// PREF: the next plane's first D levels (r into a side buffer, q into the
+// ring's q slots, which the backward sweep does not use) are issued when the
+// backward sweep starts, so the next forward sweep starts with a full ring.
+template <bool DEFER, bool TOPREG = false, bool PREF = false>
 __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const double* __restrict__ q,
                                                  double* __restrict__ z, double alpha) {
-    extern __shared__ double ring_all[];  // [slot][2][NT]
+    extern __shared__ double ring_all[];  // [slot][2][NT], then (PREF) [D][NT]
     const int tid = threadIdx.x;
     double* ring = ring_all + tid;
+    double* side = ring_all + NS * 2 * NT + tid;
+    bool prefetched = false;
     const int M = cM, TPC = cTPC;
     const long long plane = static_cast<long long>(NZ) * M;
     for (int rep = 0; rep < TPC; ++rep) {
@@ -46,11 +51,18 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
         double* rc = r + il * plane + j;
         const double* qc = q + il * plane + j;
         double* zc = z + il * plane + j;
-        for (int t = 0; t < D; ++t) {
-            cpa8(ring + (2 * t) * NT, rc + static_cast<long long>(t) * M);
-            cpa8(ring + (2 * t + 1) * NT, qc + static_cast<long long>(t) * M);
-            commit();
+        if (PREF && prefetched) {
+            wait_g<0>();
+            for (int t = 0; t < D; ++t) ring[(2 * t) * NT] = side[t * NT];
+            for (int t = 0; t < D; ++t) commit();  // keep the group count of the prefill
+        } else {
+            for (int t = 0; t < D; ++t) {
+                cpa8(ring + (2 * t) * NT, rc + static_cast<long long>(t) * M);
+                cpa8(ring + (2 * t + 1) * NT, qc + static_cast<long long>(t) * M);
+                commit();
+            }
         }
+        prefetched = false;
         double top = 0.0;
         double keep[16];
         double* zprev = z + (il - 1) * plane + j;  // DEFER: the previous plane's z
@@ -70,6 +82,16 @@ __global__ void __launch_bounds__(NT) k_pattern(double* __restrict__ r, const do
         }
         wait_g<0>();
         __threadfence_block();
+        if (PREF && rep + 1 < TPC && il + 1 < M) {  // next plane's first levels
+            const double* rn = r + (il + 1) * plane + j;
+            const double* qn = q + (il + 1) * plane + j;
+            for (int t = 0; t < D; ++t) {
+                cpa8(side + t * NT, rn + static_cast<long long>(t) * M);
+                cpa8(ring + (2 * t + 1) * NT, qn + static_cast<long long>(t) * M);
+            }
+            commit();
+            prefetched = true;
+        }
         const int kb = TOPREG ? NZ - 17 : NZ - 2;  // first level re-read from memory
         for (int t = 0; t < D; ++t) {
             const int k = kb - t;
@@ -116,11 +138,12 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int defer = 0; defer < 3; ++defer)
+    for (int defer = 0; defer < 4; ++defer)
     for (int ctas : {2, 3, 4}) {
-        auto kern = defer == 2 ? k_pattern<false, true> : defer ? k_pattern<true> : k_pattern<false>;
+        auto kern = defer == 3 ? k_pattern<false, false, true>
+                  : defer == 2 ? k_pattern<false, true> : defer ? k_pattern<true> : k_pattern<false>;
         size_t smem = 233472 / (ctas + 1) - 1024 + 64;  // the k_thomas_tm padding rule
-        const size_t ring = static_cast<size_t>(NS) * 2 * NT * 8;
+        const size_t ring = static_cast<size_t>(NS) * 2 * NT * 8 + (defer == 3 ? D * NT * 8 : 0);
         if (smem < ring) smem = ring;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         int occ = 0;
@@ -135,7 +158,7 @@ int main(int argc, char** argv) {
         ms /= 20;
         const double model = 4.0 * n * 8 + 2.0 * M * M * 8;  // K1's algorithmic bytes
         std::printf("%s CTAs/SM %d (occupancy %d, %d warps/SM): %.3f ms per launch = %.0f GB/s of the model\n",
-                    defer == 2 ? "top r* reg:" : defer ? "deferred z:" : "as K1:     ", ctas, occ, occ * 4, ms, model / ms / 1e6);
+                    defer == 3 ? "prefetch:  " : defer == 2 ? "top r* reg:" : defer ? "deferred z:" : "as K1:     ", ctas, occ, occ * 4, ms, model / ms / 1e6);
     }
     std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
