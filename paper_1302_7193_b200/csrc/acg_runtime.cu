@@ -15,14 +15,15 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <thread>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/acg.h"
@@ -919,6 +920,75 @@ bool host_is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// Host threads for the staged copies: persistent workers (spawning a dozen
+// threads per 32 MB chunk cost several ms per GB), one job at a time; the
+// caller copies slice 0 itself.
+class CopyPool {
+public:
+    explicit CopyPool(int workers) {
+        for (int w = 0; w < workers; ++w) th_.emplace_back([this, w] { run(w + 1); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void copy(char* dst, const char* src, size_t n) {
+        std::lock_guard<std::mutex> one_job(job_mu_);
+        const size_t parts = th_.size() + 1;
+        const size_t per = (n + parts - 1) / parts;
+        {
+            std::lock_guard<std::mutex> l(m_);
+            dst_ = dst;
+            src_ = src;
+            n_ = n;
+            per_ = per;
+            pending_ = static_cast<int>(th_.size());
+            ++gen_;
+        }
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(n, per));
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [&] { return pending_ == 0; });
+    }
+
+private:
+    void run(size_t part) {
+        unsigned long long seen = 0;
+        for (;;) {
+            char* dst;
+            const char* src;
+            size_t n, per;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                dst = dst_;
+                src = src_;
+                n = n_;
+                per = per_;
+            }
+            const size_t a = part * per, b = std::min(n, a + per);
+            if (a < b) std::memcpy(dst + a, src + a, b - a);
+            std::lock_guard<std::mutex> l(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex job_mu_, m_;
+    std::condition_variable cv_, done_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t n_ = 0, per_ = 0;
+    int pending_ = 0;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+};
+
 void par_memcpy(void* dst, const void* src, size_t n) {
     // up to 12 host threads: on the 16-core gpurun hosts a 1 GB numpy solve's
     // staged transfers took ~305 ms end to end with 8, ~292 with 12, ~302 with 16
@@ -926,21 +996,12 @@ void par_memcpy(void* dst, const void* src, size_t n) {
         const unsigned hw = std::thread::hardware_concurrency();
         return static_cast<int>(hw == 0 ? 1 : (hw > 12 ? 12 : hw));
     }();
-    const size_t per = (n + nt - 1) / nt;
     if (nt == 1 || n < (size_t(1) << 20)) {
         std::memcpy(dst, src, n);
         return;
     }
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) {
-        const size_t a = t * per, b = std::min(n, a + per);
-        if (a < b)
-            th.emplace_back([=] {
-                std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
-            });
-    }
-    std::memcpy(dst, src, std::min(n, per));
-    for (auto& x : th) x.join();
+    static CopyPool pool(nt - 1);
+    pool.copy(static_cast<char*>(dst), static_cast<const char*>(src), n);
 }
 
 void ensure_pinned(const acg_context* c) {
