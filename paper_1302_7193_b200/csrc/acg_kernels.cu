@@ -1256,7 +1256,11 @@ void launch_precondition(const SlabView<T>& v, bool fast, const T* y, T* x, Scal
 // cp.async ring, C3 K2 1.18 ms); fp32 with m % 4 == 0 k_fused_spmv_quad (four
 // columns per thread, the same ring with 16-byte quads, C4 K2 2.37 ms), other
 // even m k_fused_spmv_pair (neighbour rows loaded a level ahead); odd m
-// k_fused_spmv_tile (shared z tiles).
+// k_fused_spmv_tile (shared z tiles). Power-of-two fp64 panels narrower than
+// 512 columns split the levels over 512/m thread groups (k_fused_spmv_pair2
+// <..., KS>, C1 33.2 -> 27.6 us per iteration), and small single-slab grids
+// finish the previous sweep's reduction in the prologue (<..., CS>; the K1
+// side in k_thomas_tm<..., CS>), DESIGN.md §5.3.
 // Measured-slower kernels (one column per thread with plain or ring loads) and
 // the other ring depths were removed after round 1.
 inline bool spmv_pairs(int m) { return m % 2 == 0; }
