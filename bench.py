@@ -583,13 +583,14 @@ def run_gpu(args, cfg):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall, wall_serial = float(t[0].item()), float(t[1].item())
         nbytes = ml * m * n_z * s
-        e2e = {"value": nsolve * args.steps / wall, "unit": "iter/s",
-               "h2d_bytes_per_step": nbytes * world / args.steps,
-               "d2h_bytes_per_step": nbytes * world / args.steps + 8 * (args.steps + 1),
+        its = max(1, int(r2["iterations"]))  # = steps unless a small grid converged first
+        e2e = {"value": nsolve * its / wall, "unit": "iter/s",
+               "h2d_bytes_per_step": nbytes * world / its,
+               "d2h_bytes_per_step": nbytes * world / its + 8 * (its + 1),
                "call": "acg_field_upload_async + acg_solve + acg_field_download_async "
                        "(pinned host, copy stream beside the solve)",
                "solves": nsolve, "iterations_per_solve": r2["iterations"], "wall_s": wall,
-               "serial": {"value": args.steps / wall_serial,
+               "serial": {"value": its / wall_serial,
                           "call": "acg_field_upload + acg_solve + acg_field_download (pinned host)",
                           "wall_s": wall_serial, "split": split}}
         for x in fs + us + hf + hu:
