@@ -111,3 +111,26 @@ def test_gpu_arm_multi_rank_reexec(n, config):
     if n == 2:
         e = d["e2e"]
         assert e["value"] > 0 and e["solves"] >= 2 and e["serial"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_long_small_grid_passes_restart():
+    """Each measured pass restarts the solve: at C1 (whose residual reaches exactly
+    zero after ~1400 iterations) a 1000-step run with the per-launch timing pass
+    and a 1000-step sustained pass is valid; a single 3000-step pass is refused."""
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            pytest.skip("no GPU")
+    except Exception:
+        pytest.skip("no torch")
+    base = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--warmup", "3",
+            "--no-cpu", "--no-e2e"]
+    r = subprocess.run(base + ["--steps", "1000", "--sustain-steps", "1000"], capture_output=True,
+                       text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
+    assert d["steps"] == 1000 and d["sustained"]["steps"] == 1000 and d["roofline"]["achieved"] > 0
+    r = subprocess.run(base + ["--steps", "3000", "--sustain-steps", "0", "--no-ktime"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode != 0 and "converged" in (r.stdout + r.stderr)
